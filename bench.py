@@ -1,0 +1,454 @@
+#!/usr/bin/env python
+"""bench.py -- ME + consistency-check throughput on B200 (BASELINE.json "metric").
+
+A step = one frame t of config 4 (1920x1080, dynamic quarter mask, float32 previous
+reconstructions, K=8, S=24): for each reference d = 1..3 the whole hot path of
+SURVEY.md §8(a) -- ME (qs_me_search) with the paper's NNC -> FRMC cascade fused into the call,
+then PR (qs_project) -- through the C ABI.  value = frame pixels per second (Mpixel/s), the
+whole job over all ranks.
+
+  python bench.py [--gpus N --steps K --warmup W]            ours (CUDA path)
+  python bench.py --impl reference ...                        the CPU oracle (rank 0 only)
+
+N > 1 (torchrun, one rank per GPU): the frame is row-band sharded (rank r owns ~H/N rows,
+SURVEY.md §8(e)); each step first exchanges the newest reference's halo rows with the
+neighbouring ranks (NCCL P2P), then runs the path on its band.  Timed on the device with CUDA
+events, max over ranks.  Inputs: 24 resident frames (> L2); consecutive steps use disjoint
+frames (stride 4), so no step finds its inputs in L2 from the previous one.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ME+consistency-check Mpixel/s (1080p, 1/2/4/8 B200) and % of roofline"
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128          # B200 SM: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md, blackwell guide)
+SM_MAX_MHZ = 1965.0              # clocks.max.sm (B200_PROFILING.md)
+OPS_PER_UNIT = 8                 # D (2) + H (2) + V (2) + argmin (2) per (pixel, candidate)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--check", default="nnc_frmc", choices=["nnc_frmc", "none"])
+    ap.add_argument("--frames", type=int, default=24)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--variants", action="store_true", help="also time the CC variants (RME, RMC, FRMC, NNC->FRMC)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# Clocks during the timed region (NVML, sampled every 20 ms)
+# ---------------------------------------------------------------------------
+_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self._h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            try:
+                props = torch.cuda.get_device_properties(device_index)
+                bus = "%08x:%02x:%02x.0" % (props.pci_domain_id, props.pci_bus_id, props.pci_device_id)
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self._nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._h = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self._h is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._h is not None:
+            self._t.join()
+
+    def summary(self):
+        if self._h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples),
+                "reasons": [n for b, n in _REASONS.items() if self.reasons & b and b != 0x1]}
+
+
+# ---------------------------------------------------------------------------
+# Inputs
+# ---------------------------------------------------------------------------
+def make_frames(cfg: int, n_frames: int):
+    import synth
+    seq = synth.make_sequence(cfg)
+    frames = []
+    for t in range(n_frames):
+        m = seq.mask(t)
+        frames.append(dict(cur=(seq.frame(t) * m).astype(np.uint8), mask=m, ref=seq.ref(t)))
+    return seq, frames
+
+
+def step_order(n_frames: int, steps: int):
+    """Frames t >= 3 (three references) visited with stride 4 so consecutive steps share no frame."""
+    ts = list(range(3, n_frames))
+    order = []
+    for start in range(4):
+        order += ts[start::4]
+    return [order[i % len(order)] for i in range(steps)]
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2203_09200_b200 as qs
+    from paper_2203_09200_b200 import rowband
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    W, H, K, S = cfg.w, cfg.h, cfg.K, cfg.S
+    f32 = cfg.ref_f32
+    band = rowband.band_of(rank, world, H, rowband.halo_rows(S, K))
+    seq, frames = make_frames(args.config, args.frames)
+
+    # Device-resident band buffers (row i = global row band.b0 + i).
+    def dplane(a):
+        return qs.to_plane(a[band.b0:band.b1], dev)
+
+    dfr = []
+    for fr in frames:
+        ref = dplane(fr["ref"])
+        if world > 1:   # the reconstruction exists only for owned rows until the halo exchange
+            ref[:band.y0 - band.b0] = float("nan") if f32 else 0
+            ref[band.y1 - band.b0:] = float("nan") if f32 else 0
+        dfr.append(dict(cur=dplane(fr["cur"]), mask=dplane(fr["mask"]), ref=ref))
+    if world > 1:       # each frame's reference halo, as it would have arrived when it was newest
+        for d in dfr:
+            rowband.exchange_halo(d["ref"], band)
+    torch.cuda.synchronize()
+
+    roi = qs.make_roi(W, H, band.y0, band.y1, band.b0, band.rows)
+    prm = qs.make_params(K=K, S=S, min_support=8, ssd=cfg.ssd, ref_f32=f32)
+    checks = qs.make_checks() if args.check == "nnc_frmc" else None
+    fields = [qs.Field.alloc(band.rows, W, f32, dev) for _ in range(3)]
+    wss = [qs.workspace(roi, prm, dev) for _ in range(3)]
+    acc_s, acc_c = qs.alloc_acc(band.rows, W, dev)
+    evals = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def step(t):
+        if world > 1:
+            rowband.exchange_halo(dfr[t - 1]["ref"], band)
+        acc_s.zero_()
+        acc_c.zero_()
+        for d in (1, 2, 3):
+            fr, past = dfr[t], dfr[t - d]
+            qs.qs_me_search(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1], fuse=checks,
+                            eval_count=evals, ws=wss[d - 1])
+            qs.qs_project(fields[d - 1], past["cur"], past["mask"], roi, acc_s, acc_c)
+
+    order = step_order(args.frames, args.warmup + args.steps)
+    for t in order[:args.warmup]:
+        step(t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    qs.qs_profile_reset()
+    qs.qs_profile_enable(True)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0.record()
+        for t in order[args.warmup:]:
+            step(t)
+        t1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    qs.qs_profile_enable(False)
+    ms = t0.elapsed_time(t1)
+    prof = {k: qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS}
+    launches = sum(n for _, n in prof.values())
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = args.steps * W * H / (ms / 1e3) / 1e6
+
+    # Roofline of the dominant kernel (me_box).
+    me_ms, me_n = prof["me_box"]
+    n_cand = (2 * S + 1) ** 2
+    me_rows = min(H, band.y1 + 2) - max(0, band.y0 - 2)
+    units_per_launch = me_rows * W * n_cand
+    achieved = OPS_PER_UNIT * units_per_launch / (me_ms / me_n / 1e3) / 1e12 if me_n else None
+    peak = SM_COUNT * FP32_LANES_PER_SM * SM_MAX_MHZ * 1e6 / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "me_box_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "me_box", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "ops_per_unit": OPS_PER_UNIT, "units_per_launch": units_per_launch,
+                "avg_launch_ms": me_ms / me_n if me_n else None,
+                "share_of_step": me_ms / ms if ms else None,
+                "peak_basis": "148 SM x 128 FP32 lanes x 1965 MHz (guide unit counts and max clock)"}
+    kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W, H, order)
+
+    out = None
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f32" if f32 else "u8->f32(exact)", "data": "synthetic",
+               "config": {"workload": cfg.name, "frame": f"{W}x{H}", "K": K, "S": S, "refs": 3,
+                          "mask": "dynamic" if cfg.dynamic else "fixed", "check": args.check,
+                          "parallelism": f"rowband{world}" if world > 1 else "single",
+                          "l2": "24 resident frames (~345 MB > 126 MB L2); consecutive steps use disjoint frames"},
+               "roofline": roofline, "kernel_ms_per_step": kernel_ms, "gpu_launches": launches,
+               "clocks": clk.summary(), "e2e": e2e, "impl": "ours"}
+        if args.variants:
+            out["cc_variants_ms_per_frame"] = run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(seq, frames, cfg)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W, H, order):
+    """Same metric through the C ABI with HOST inputs: each step copies its frames' planes from
+    pinned host memory, runs the path, and reads the projection planes back."""
+    f32 = prm.ref_type == qs.QS_REF_F32
+
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a[band.b0:band.b1])).pin_memory()
+        return t
+
+    host = [dict(cur=pinned(fr["cur"]), mask=pinned(fr["mask"]), ref=pinned(fr["ref"])) for fr in frames]
+    slots = [dict(cur=qs.pitched(band.rows, W, torch.uint8, dev), mask=qs.pitched(band.rows, W, torch.uint8, dev),
+                  ref=qs.pitched(band.rows, W, torch.float32 if f32 else torch.uint8, dev)) for _ in range(4)]
+    fields = [qs.Field.alloc(band.rows, W, f32, dev) for _ in range(3)]
+    wss = [qs.workspace(roi, prm, dev) for _ in range(3)]
+    acc_s, acc_c = qs.alloc_acc(band.rows, W, dev)
+    out_s = torch.empty((band.rows, W), dtype=torch.int32).pin_memory()
+    out_c = torch.empty((band.rows, W), dtype=torch.uint8).pin_memory()
+    h2d = d2h = 0
+
+    def step(t, count=False):
+        nonlocal h2d, d2h
+        for j in range(4):          # slot j holds frame t - j
+            src = host[t - j]
+            for k in ("cur", "mask") + (("ref",) if j > 0 else ()):
+                slots[j][k].copy_(src[k], non_blocking=True)
+                if count:
+                    h2d += src[k].numel() * src[k].element_size()
+        acc_s.zero_()
+        acc_c.zero_()
+        for d in (1, 2, 3):
+            qs.qs_me_search(slots[0]["cur"], slots[0]["mask"], slots[d]["ref"], roi, prm, fields[d - 1],
+                            fuse=checks, ws=wss[d - 1])
+            qs.qs_project(fields[d - 1], slots[d]["cur"], slots[d]["mask"], roi, acc_s, acc_c)
+        out_s.copy_(acc_s, non_blocking=True)
+        out_c.copy_(acc_c, non_blocking=True)
+        if count:
+            d2h += out_s.numel() * 4 + out_c.numel()
+
+    for t in order[:args.warmup]:
+        step(t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for t in order[args.warmup:]:
+        step(t, count=True)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"value": round(args.steps * W * H / (ms / 1e3) / 1e6, 3), "unit": "Mpixel/s",
+            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+            "ms_per_step": round(ms / args.steps, 4)}
+
+
+def run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32):
+    """GPU analogue of Table 3's CC column: per-frame check time for each variant (3 references)."""
+    res = {}
+    t = 7
+    for name in ("nnc_frmc", "frmc", "rme", "rmc"):
+        tot = 0.0
+        for d in (1, 2, 3):
+            fr, past = dfr[t], dfr[t - d]
+            qs.qs_me_search(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1], ws=wss[d - 1])
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            if name == "nnc_frmc":
+                qs.qs_nnc(fields[d - 1], roi)
+                qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1])
+            elif name == "frmc":
+                qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1])
+            elif name == "rme":
+                qs.qs_reverse_check(qs.QS_RME, fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1],
+                                    ws=wss[d - 1])
+            else:
+                qs.qs_reverse_check(qs.QS_RMC, fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1])
+            b.record()
+            torch.cuda.synchronize()
+            tot += a.elapsed_time(b)
+        res[name] = round(tot, 3)
+    return res
+
+
+# ---------------------------------------------------------------------------
+# The oracle: cpu_baseline (inside our line) and the --impl reference arm
+# ---------------------------------------------------------------------------
+def oracle_sample(frames, cfg, t, rows):
+    """The oracle on a bounded sample: output rows `rows` of frame t, references d = 1..3:
+    ME -> NNC -> FRMC -> PR on those rows (timed).  The 2 halo rows of vectors NNC reads are
+    computed untimed, as a full-frame run computes them once for the neighbouring rows.
+    Returns the timed seconds."""
+    import oracle
+    K, S = cfg.K, cfg.S
+    H = frames[t]["cur"].shape[0]
+    y0, y1 = rows
+    sec = 0.0
+    s = c = None
+    for d in (1, 2, 3):
+        cur, msk, ref = frames[t]["cur"], frames[t]["mask"], frames[t - d]["ref"]
+        kw = dict(K=K, S=S, min_support=8)
+        t0 = time.perf_counter()
+        f = oracle.me_search(cur, msk, ref, rows=(y0, y1), **kw)
+        sec += time.perf_counter() - t0
+        for hr in ((max(0, y0 - 2), y0), (y1, min(H, y1 + 2))):
+            if hr[0] < hr[1]:
+                h = oracle.me_search(cur, msk, ref, rows=hr, **kw)
+                for k in f:
+                    f[k][hr[0]:hr[1]] = h[k][hr[0]:hr[1]]
+        t0 = time.perf_counter()
+        f["status"] = oracle.nnc(f, 1, rows=(y0, y1))
+        f["status"], _ = oracle.frmc(cur, msk, ref, f, rows=(y0, y1), **kw)
+        s, c = oracle.project(f, frames[t - d]["cur"], frames[t - d]["mask"], s, c, rows=(y0, y1))
+        sec += time.perf_counter() - t0
+    return sec
+
+
+def cpu_baseline(seq, frames, cfg, rows=None):
+    import oracle
+    oracle.build()
+    H = cfg.h
+    rows = rows or (H // 2, H // 2 + 6)
+    sec = oracle_sample(frames, cfg, 3, rows)
+    px = (rows[1] - rows[0]) * cfg.w
+    return {"value": round(px / sec / 1e6, 6), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
+            "sample": f"frame t=3 of {cfg.name}, output rows {rows[0]}-{rows[1] - 1} ({rows[1] - rows[0]} of {H}), "
+                      f"d=1..3, ME on rows +-2 (NNC halo) -> NNC -> FRMC -> PR; single-threaded C oracle",
+            "seconds": round(sec, 3)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    seq, frames = make_frames(args.config, 8)
+    import oracle
+    oracle.build()
+    H, W = cfg.h, cfg.w
+    rng = np.random.default_rng(0)
+    rows_per_step = 1
+    def sample_rows():
+        y = int(rng.integers(0, H - rows_per_step + 1))
+        return (y, y + rows_per_step)
+    for _ in range(args.warmup):
+        oracle_sample(frames, cfg, 3 + rng.integers(0, 5), sample_rows())
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += oracle_sample(frames, cfg, 3 + int(rng.integers(0, 5)), sample_rows())
+    value = args.steps * rows_per_step * W / tot / 1e6
+    line = {"metric": METRIC, "value": round(value, 6), "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg.ref_f32 else "u8", "data": "synthetic",
+            "config": {"workload": cfg.name, "frame": f"{W}x{H}", "K": cfg.K, "S": cfg.S, "refs": 3,
+                       "check": "nnc_frmc", "parallelism": "cpu-1-thread"},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(value, 6), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
+                             "sample": f"per step: {rows_per_step} random output row of a random frame t in 3..7, "
+                                       f"d=1..3, ME rows +-2 -> NNC -> FRMC -> PR"},
+            "e2e": {"value": round(value, 6), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        line = run_reference(args)
+    else:
+        line = run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,272 @@
+// checks.cu -- the consistency checks and the projection on sm_100a.
+//   K5 nnc       NNC (§3.1.2, Eq. (1); R14, R15)
+//   K3/K4 revgrid FRMC and RMC: reverse costs
+//                rc(x = p+v, u = -v + delta) over a delta grid (R9, R11, R12)
+//   K4 rme_decide RME (R10) from the dense reverse keys of me_box
+//   K6 project   PR (§2.2; R18)
+#include <cmath>
+
+#include "qs_internal.cuh"
+
+namespace qs {
+namespace {
+
+__device__ __forceinline__ bool checkable(uint8_t s) { return s == kCandidate || s == kAccepted; }
+
+// ---------------------------------------------------------------------------
+// NNC.  Block = 32 x 8 outputs.  Shared: the field with a 2-pixel halo, then
+// the filtered field (Eq. (1)) with a 1-pixel halo; then the 4-neighbour rule.
+// ---------------------------------------------------------------------------
+constexpr int kNX = 32, kNY = 8;
+
+// Lower median of the valid values among v[0..8] (invalid entries carry +1000
+// and sort last): sort ascending, take index (n-1)/2.
+__device__ __forceinline__ int lower_median9(int (&v)[9], int n) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8 - i; ++j) {
+            const int a = v[j], b = v[j + 1];
+            v[j] = min(a, b);
+            v[j + 1] = max(a, b);
+        }
+    int r = v[0];
+#pragma unroll
+    for (int i = 1; i < 9; ++i)
+        if (i == (n - 1) / 2) r = v[i];
+    return r;
+}
+
+__global__ void __launch_bounds__(kNX * kNY) nnc_kernel(FieldView f, int W, int H, int buf_y0, int buf_rows,
+                                                          int y0, int y1, int threshold) {
+    __shared__ int sa[kNY + 4][kNX + 4], sb[kNY + 4][kNX + 4];
+    __shared__ uint8_t sv[kNY + 4][kNX + 4];
+    __shared__ int fa[kNY + 2][kNX + 2], fb[kNY + 2][kNX + 2];
+    const int tx0 = blockIdx.x * kNX, ty0 = y0 + blockIdx.y * kNY;
+    const int tid = threadIdx.y * kNX + threadIdx.x;
+    for (int i = tid; i < (kNY + 4) * (kNX + 4); i += kNX * kNY) {
+        const int r = i / (kNX + 4), c = i % (kNX + 4);
+        const int gy = ty0 - 2 + r, gx = tx0 - 2 + c;
+        int a = 0, b = 0;
+        uint8_t v = 0;
+        if (gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= buf_y0 && gy < buf_y0 + buf_rows) {
+            const int64_t fi = (int64_t)(gy - buf_y0) * f.pitch + gx;
+            v = f.status[fi] >= kCandidate;
+            a = f.alpha[fi];
+            b = f.beta[fi];
+        }
+        sa[r][c] = a;
+        sb[r][c] = b;
+        sv[r][c] = v;
+    }
+    __syncthreads();
+    for (int i = tid; i < (kNY + 2) * (kNX + 2); i += kNX * kNY) {
+        const int r = i / (kNX + 2) + 1, c = i % (kNX + 2) + 1;   // coords in the 2-halo arrays
+        int va[9], vb[9], n = 0;
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int k = (dy + 1) * 3 + (dx + 1);
+                const bool ok = sv[r + dy][c + dx];
+                va[k] = ok ? sa[r + dy][c + dx] : 1000;
+                vb[k] = ok ? sb[r + dy][c + dx] : 1000;
+                n += ok;
+            }
+        int ma = 0, mb = 0;
+        if (sv[r][c]) {
+            ma = lower_median9(va, n);
+            mb = lower_median9(vb, n);
+        }
+        fa[r - 1][c - 1] = ma;
+        fb[r - 1][c - 1] = mb;
+    }
+    __syncthreads();
+    const int gx = tx0 + threadIdx.x, gy = ty0 + threadIdx.y;
+    if (gx >= W || gy >= y1) return;
+    const int r = threadIdx.y + 2, c = threadIdx.x + 2;   // 2-halo coords
+    const int64_t fi = (int64_t)(gy - buf_y0) * f.pitch + gx;
+    const uint8_t st = f.status[fi];
+    if (!checkable(st)) return;
+    const int ca = fa[r - 1][c - 1], cb = fb[r - 1][c - 1];
+    bool reject = false;
+    const int NBR[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int rr = r + NBR[k][0], cc = c + NBR[k][1];
+        if (!sv[rr][cc]) continue;   // out of frame or not valid: skipped (R15)
+        const int d = abs(ca - fa[rr - 1][cc - 1]) + abs(cb - fb[rr - 1][cc - 1]);
+        if (d > threshold) reject = true;
+    }
+    f.status[fi] = reject ? kRejected : kAccepted;
+}
+
+// ---------------------------------------------------------------------------
+// Reverse-cost grid (FRMC / RMC).  One thread per field entry.  Each reverse
+// cost is summed in the definition's row-major order (R9, R23), so the f32
+// decisions are those of the oracle given the same field; the delta loop may
+// stop at the first strictly smaller mean (the decision is "reject iff any",
+// R11) while the evaluation counter reports the definitional |delta set| (R17).
+// ---------------------------------------------------------------------------
+struct DeltaSet {
+    int n;              // 0 => full range [lo, hi]^2
+    int lo, hi;
+    int8_t v[16];
+};
+
+__global__ void revgrid_kernel(RevGridArgs a, DeltaSet ds) {
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = a.y0 + blockIdx.y;
+    unsigned long long my_evals = 0;
+    if (gx < a.W && gy < a.y1) {
+        const int64_t fi = (int64_t)(gy - a.buf_y0) * a.f.pitch + gx;
+        const uint8_t st = a.f.status[fi];
+        if (checkable(st)) {
+            const int va = a.f.alpha[fi], vb = a.f.beta[fi];
+            const int xy = gy + va, xx = gx + vb;
+            const int n0 = a.f.count[fi];
+            const float e0f = a.ref_f32 ? reinterpret_cast<const float *>(a.f.err)[fi] : 0.f;
+            const uint32_t e0u = a.ref_f32 ? 0u : reinterpret_cast<const uint32_t *>(a.f.err)[fi];
+            const float m0 = a.ref_f32 ? __fdiv_rn(e0f, (float)n0) : 0.f;
+            const int KL = a.K / 2;
+            const int nd = ds.n ? ds.n : (ds.hi - ds.lo + 1);
+            bool reject = false;
+            for (int iy = 0; iy < nd && !reject; ++iy) {
+                const int dy = ds.n ? ds.v[iy] : ds.lo + iy;
+                for (int ix = 0; ix < nd && !reject; ++ix) {
+                    const int dx = ds.n ? ds.v[ix] : ds.lo + ix;
+                    if (dy == 0 && dx == 0) continue;
+                    const int uy = -va + dy, ux = -vb + dx;
+                    int n = 0;
+                    uint32_t eu = 0;
+                    float ef = 0.f;
+                    for (int oy = -KL; oy < a.K - KL; ++oy) {
+                        const int qy = xy + oy, sy = qy + uy;
+                        if (qy < 0 || qy >= a.H || sy < 0 || sy >= a.H) continue;
+                        if (qy < a.buf_y0 || qy >= a.buf_y0 + a.buf_rows) continue;   // never for valid rois
+                        if (sy < a.buf_y0 || sy >= a.buf_y0 + a.buf_rows) continue;
+                        const int64_t qr = qy - a.buf_y0, sr = sy - a.buf_y0;
+                        for (int ox = -KL; ox < a.K - KL; ++ox) {
+                            const int qx = xx + ox, sx = qx + ux;
+                            if (qx < 0 || qx >= a.W || sx < 0 || sx >= a.W) continue;
+                            if (!a.mask.p[sr * a.mask.pitch + sx]) continue;
+                            const int c = a.cur.p[sr * a.cur.pitch + sx];
+                            if (a.ref_f32) {
+                                const float rv = reinterpret_cast<const float *>(a.ref.p + qr * a.ref.pitch)[qx];
+                                const float d = __fsub_rn((float)c, rv);
+                                ef = __fadd_rn(ef, a.ssd ? __fmul_rn(d, d) : fabsf(d));
+                            } else {
+                                const int d = c - (int)a.ref.p[qr * a.ref.pitch + qx];
+                                eu += (uint32_t)(a.ssd ? d * d : (d < 0 ? -d : d));
+                            }
+                            ++n;
+                        }
+                    }
+                    if (n < a.min_support) continue;   // SENTINEL never rejects (R11)
+                    if (a.ref_f32) {
+                        if (__fdiv_rn(ef, (float)n) < m0) reject = true;
+                    } else {
+                        if ((unsigned long long)eu * (unsigned)n0 < (unsigned long long)e0u * (unsigned)n) reject = true;
+                    }
+                }
+            }
+            my_evals = (unsigned long long)nd * nd;
+            a.f.status[fi] = reject ? kRejected : kAccepted;
+        }
+    }
+    if (a.evals) {
+        // warp-aggregate the definitional count
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) my_evals += __shfl_down_sync(0xffffffffu, my_evals, o);
+        if ((threadIdx.x & 31) == 0 && my_evals) atomicAdd(a.evals, my_evals);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// RME decision from the dense reverse keys (argmin over u in rank order).
+// ---------------------------------------------------------------------------
+__global__ void rme_decide_kernel(RmeDecideArgs a) {
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = a.y0 + blockIdx.y;
+    unsigned long long my_evals = 0;
+    if (gx < a.W && gy < a.y1) {
+        const int64_t fi = (int64_t)(gy - a.buf_y0) * a.f.pitch + gx;
+        if (checkable(a.f.status[fi])) {
+            const int va = a.f.alpha[fi], vb = a.f.beta[fi];
+            const int xy = gy + va, xx = gx + vb;
+            const unsigned long long key =
+                a.keys[(int64_t)(xy - (a.y0 - a.S)) * a.key_pitch + (xx + a.S)];
+            bool ok = false;
+            if (key != ~0ull) {
+                const int pk = __ldg(a.canon + (int)(key & 0xffffffffu));
+                const int ua = (int)(int8_t)(pk & 0xff), ub = (int)(int8_t)((pk >> 8) & 0xff);
+                ok = (ua == -va) && (ub == -vb);
+            }
+            a.f.status[fi] = ok ? kAccepted : kRejected;
+            my_evals = (unsigned long long)a.n_cand;
+        }
+    }
+    if (a.evals) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) my_evals += __shfl_down_sync(0xffffffffu, my_evals, o);
+        if ((threadIdx.x & 31) == 0 && my_evals) atomicAdd(a.evals, my_evals);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Projection.
+// ---------------------------------------------------------------------------
+__global__ void project_kernel(ProjectArgs a) {
+    const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = a.y0 + blockIdx.y;
+    if (gx >= a.W || gy >= a.y1) return;
+    const int64_t r = gy - a.buf_y0;
+    const int64_t fi = r * a.f.pitch + gx;
+    if (a.f.status[fi] != kAccepted) return;
+    const int qy = gy + a.f.alpha[fi], qx = gx + a.f.beta[fi];
+    if (qy < 0 || qy >= a.H || qx < 0 || qx >= a.W) return;
+    if (qy < a.buf_y0 || qy >= a.buf_y0 + a.buf_rows) return;   // never for valid rois
+    const int64_t qr = qy - a.buf_y0;
+    if (!a.past_mask.p[qr * a.past_mask.pitch + qx]) return;
+    const int64_t ai = r * a.acc_pitch + gx;
+    a.sum[ai] += a.past_val.p[qr * a.past_val.pitch + qx];
+    a.cnt[ai] += 1;
+}
+
+}  // namespace
+
+cudaError_t launch_nnc(FieldView f, int W, int H, int buf_y0, int buf_rows, int y0, int y1, int threshold,
+                       cudaStream_t s) {
+    if (y1 <= y0) return cudaSuccess;
+    dim3 blk(kNX, kNY), grd((W + kNX - 1) / kNX, (y1 - y0 + kNY - 1) / kNY);
+    nnc_kernel<<<grd, blk, 0, s>>>(f, W, H, buf_y0, buf_rows, y0, y1, threshold);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_revgrid(const RevGridArgs &a, cudaStream_t s) {
+    if (a.y1 <= a.y0) return cudaSuccess;
+    DeltaSet ds{};
+    ds.n = a.n_dy;
+    ds.lo = a.full_lo;
+    ds.hi = a.full_hi;
+    for (int i = 0; i < a.n_dy && i < 16; ++i) ds.v[i] = a.dys_host[i];
+    dim3 blk(128), grd((a.W + 127) / 128, a.y1 - a.y0);
+    revgrid_kernel<<<grd, blk, 0, s>>>(a, ds);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rme_decide(const RmeDecideArgs &a, cudaStream_t s) {
+    if (a.y1 <= a.y0) return cudaSuccess;
+    dim3 blk(128), grd((a.W + 127) / 128, a.y1 - a.y0);
+    rme_decide_kernel<<<grd, blk, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_project(const ProjectArgs &a, cudaStream_t s) {
+    if (a.y1 <= a.y0) return cudaSuccess;
+    dim3 blk(128), grd((a.W + 127) / 128, a.y1 - a.y0);
+    project_kernel<<<grd, blk, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace qs

@@ -1,0 +1,561 @@
+// qs_api.cu -- the extern "C" boundary of libqs (include/qs.h): argument
+// validation, the one-time candidate tables, and the launch sequences.
+// Everything here is host code; every step of the path runs in the kernels of
+// me_box.cu and checks.cu.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "qs_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    return fail(QS_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------------------
+// Candidate tables: rank order (|a|+|b|, a, b) ascending (R7).
+// ---------------------------------------------------------------------------
+std::mutex g_tab_mu;
+std::map<std::pair<int, int>, qs::CandTables *> g_tabs;
+
+// ---------------------------------------------------------------------------
+// Profiler: CUDA events around each launch, on the launch stream.
+// ---------------------------------------------------------------------------
+enum ProfKernel { P_ME_BOX = 0, P_FINALIZE, P_NNC, P_REVGRID, P_RME_DECIDE, P_PROJECT, P_COUNT };
+const char *kProfNames[P_COUNT] = {"me_box", "finalize", "nnc", "revgrid", "rme_decide", "project"};
+
+struct ProfRec {
+    int kernel;
+    cudaEvent_t start, stop;
+};
+
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<ProfRec> recs;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        return e;
+    }
+} g_prof;
+
+// RAII bracket: records start on construction and stop on destruction when enabled.
+struct ProfScope {
+    int kernel;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(int k, cudaStream_t st) : kernel(k), s(st) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        if (!g_prof.on) return;
+        a = g_prof.get();
+        b = g_prof.get();
+        if (a && b) cudaEventRecord(a, s);
+    }
+    ~ProfScope() {
+        if (!a || !b) return;
+        cudaEventRecord(b, s);
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.recs.push_back({kernel, a, b});
+    }
+};
+
+}  // namespace
+
+namespace qs {
+
+const CandTables *cand_tables(int S, const char **err) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { *err = "cudaGetDevice failed"; return nullptr; }
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    auto it = g_tabs.find({dev, S});
+    if (it != g_tabs.end()) return it->second;
+    std::vector<std::pair<int, int>> v;
+    for (int a = -S; a <= S; ++a)
+        for (int b = -S; b <= S; ++b) v.push_back({a, b});
+    std::stable_sort(v.begin(), v.end(), [](const std::pair<int, int> &x, const std::pair<int, int> &y) {
+        const int lx = std::abs(x.first) + std::abs(x.second), ly = std::abs(y.first) + std::abs(y.second);
+        if (lx != ly) return lx < ly;
+        if (x.first != y.first) return x.first < y.first;
+        return x.second < y.second;
+    });
+    const int n = (int)v.size();
+    std::vector<int32_t> canon(n), chunked;
+    for (int r = 0; r < n; ++r) canon[r] = (v[r].first & 0xff) | ((v[r].second & 0xff) << 8);
+    const int n_chunks = (2 * S + 1 + kChunkRows - 1) / kChunkRows;
+    std::vector<int32_t> off(n_chunks + 1, 0);
+    for (int c = 0; c < n_chunks; ++c) {
+        const int alo = -S + c * kChunkRows, ahi = std::min(S, alo + kChunkRows - 1);
+        off[c] = (int)chunked.size();
+        for (int r = 0; r < n; ++r)
+            if (v[r].first >= alo && v[r].first <= ahi) chunked.push_back(canon[r] | (r << 16));
+    }
+    off[n_chunks] = (int)chunked.size();
+    auto *t = new CandTables;
+    t->S = S;
+    t->n = n;
+    t->n_chunks = n_chunks;
+    if (cudaMalloc(&t->canon, sizeof(int32_t) * n) != cudaSuccess ||
+        cudaMalloc(&t->chunked, sizeof(int32_t) * n) != cudaSuccess ||
+        cudaMalloc(&t->chunk_off, sizeof(int32_t) * (n_chunks + 1)) != cudaSuccess ||
+        cudaMemcpy(t->canon, canon.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(t->chunked, chunked.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(t->chunk_off, off.data(), sizeof(int32_t) * (n_chunks + 1), cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+        *err = "cudaMalloc/cudaMemcpy of the candidate tables failed";
+        delete t;
+        return nullptr;
+    }
+    g_tabs[{dev, S}] = t;
+    return t;
+}
+
+}  // namespace qs
+
+namespace {
+
+using namespace qs;
+
+struct Roi {
+    int W, H, y0, y1, b0, br;
+};
+
+int check_roi(const qs_roi *roi, Roi *r) {
+    if (!roi) return fail(QS_EINVAL, "roi is NULL (it carries the frame size)");
+    r->W = roi->frame_w;
+    r->H = roi->frame_h;
+    r->y0 = roi->y_begin;
+    r->y1 = roi->y_end;
+    r->b0 = roi->buf_y0;
+    r->br = roi->buf_rows;
+    if (r->W <= 0 || r->H <= 0 || (r->W & 1) || (r->H & 1))
+        return fail(QS_EDIM, "frame %dx%d: quarter sampling needs positive even dimensions", r->W, r->H);
+    if (r->y0 < 0 || r->y1 > r->H || r->y0 > r->y1) return fail(QS_EDIM, "rows [%d,%d) outside frame of %d", r->y0, r->y1, r->H);
+    if (r->b0 < 0 || r->br < 0 || r->b0 + r->br > r->H)
+        return fail(QS_EDIM, "buffer rows [%d,%d) outside frame of %d", r->b0, r->b0 + r->br, r->H);
+    return QS_OK;
+}
+
+// Rows [lo, hi) clipped to the frame must be held by the buffer window.
+int need_rows(const Roi &r, int lo, int hi, const char *what) {
+    lo = std::max(lo, 0);
+    hi = std::min(hi, r.H);
+    if (lo >= hi) return QS_OK;
+    if (lo < r.b0 || hi > r.b0 + r.br)
+        return fail(QS_EDIM, "%s needs rows [%d,%d) but the buffers hold [%d,%d)", what, lo, hi, r.b0, r.b0 + r.br);
+    return QS_OK;
+}
+
+int check_params(const qs_me_params *p) {
+    if (!p) return fail(QS_EINVAL, "params is NULL");
+    if (p->K_h != p->K_w || p->K_h < 1 || p->K_h > 9)
+        return fail(QS_EINVAL, "template %dx%d: this build supports square K in [1,9]", p->K_h, p->K_w);
+    if (p->S < 0 || p->S > 32) return fail(QS_EINVAL, "S=%d outside [0,32]", p->S);
+    if (p->min_support < 1) return fail(QS_EINVAL, "min_support=%d < 1", p->min_support);
+    if (p->err != QS_SAD && p->err != QS_SSD) return fail(QS_EINVAL, "err=%d", p->err);
+    if (p->ref_type != QS_REF_U8 && p->ref_type != QS_REF_F32) return fail(QS_EINVAL, "ref_type=%d", p->ref_type);
+    return QS_OK;
+}
+
+int check_plane(const void *ptr, int64_t pitch, int64_t min_pitch, const char *name) {
+    if (!ptr) return fail(QS_EINVAL, "%s is NULL", name);
+    if (!aligned16(ptr) || (pitch & 15)) return fail(QS_EALIGN, "%s: base and pitch must be 16-byte aligned", name);
+    if (pitch < min_pitch) return fail(QS_EDIM, "%s: pitch %lld < %lld", name, (long long)pitch, (long long)min_pitch);
+    return QS_OK;
+}
+
+int check_field(const qs_field *f, int W, bool need_err_count) {
+    if (!f) return fail(QS_EINVAL, "field is NULL");
+    if (!f->alpha || !f->beta || !f->status || (need_err_count && (!f->err || !f->count)))
+        return fail(QS_EINVAL, "field plane is NULL");
+    if (f->pitch < W) return fail(QS_EDIM, "field pitch %lld < width %d", (long long)f->pitch, W);
+    if (f->err && (reinterpret_cast<uintptr_t>(f->err) & 3)) return fail(QS_EALIGN, "field err plane not 4-byte aligned");
+    return QS_OK;
+}
+
+FieldView view(const qs_field *f) { return FieldView{f->alpha, f->beta, f->err, f->count, f->status, f->pitch}; }
+
+size_t me_keys_bytes(const Roi &r) {
+    return sizeof(unsigned long long) * (size_t)std::max(0, std::min(r.H, r.y1 + 2) - std::max(0, r.y0 - 2)) * r.W;
+}
+size_t rme_keys_bytes(const Roi &r, int S) {
+    return sizeof(unsigned long long) * (size_t)(r.y1 - r.y0 + 2 * S) * (size_t)(r.W + 2 * S);
+}
+
+BoxArgs box_args(const Roi &r, const uint8_t *cur, const uint8_t *mask, int64_t cur_pitch, const void *ref,
+                 int64_t ref_pitch, const qs_me_params *p, const CandTables *t) {
+    BoxArgs a{};
+    a.cur = Plane{cur, cur_pitch};
+    a.mask = Plane{mask, cur_pitch};
+    a.ref = Plane{static_cast<const uint8_t *>(ref), ref_pitch};
+    a.ref_f32 = p->ref_type == QS_REF_F32;
+    a.W = r.W;
+    a.H = r.H;
+    a.buf_y0 = r.b0;
+    a.buf_rows = r.br;
+    a.S = p->S;
+    a.min_support = p->min_support;
+    a.n_chunks = t->n_chunks;
+    a.chunked = t->chunked;
+    a.chunk_off = t->chunk_off;
+    return a;
+}
+
+int check_offsets(const int8_t *offs, int n, int S) {
+    if (!offs || n < 1 || n > 15) return fail(QS_EINVAL, "offsets: need 1..15 entries");
+    bool has0 = false;
+    for (int i = 0; i < n; ++i) {
+        if (offs[i] == 0) has0 = true;
+        if (offs[i] < -S || offs[i] > S) return fail(QS_EINVAL, "offset %d outside [-S,S] (S=%d)", offs[i], S);
+    }
+    if (!has0) return fail(QS_EINVAL, "offsets must contain 0");
+    return QS_OK;
+}
+
+int run_frmc(const Roi &r, const uint8_t *cur, const uint8_t *mask, int64_t cur_pitch, const void *ref,
+             int64_t ref_pitch, const qs_me_params *p, const int8_t *offs, int n_offs, int full, qs_field *io,
+             unsigned long long *evals, cudaStream_t s) {
+    RevGridArgs a{};
+    a.cur = Plane{cur, cur_pitch};
+    a.mask = Plane{mask, cur_pitch};
+    a.ref = Plane{static_cast<const uint8_t *>(ref), ref_pitch};
+    a.ref_f32 = p->ref_type == QS_REF_F32;
+    a.ssd = p->err == QS_SSD;
+    a.K = p->K_h;
+    a.W = r.W;
+    a.H = r.H;
+    a.buf_y0 = r.b0;
+    a.buf_rows = r.br;
+    a.min_support = p->min_support;
+    a.y0 = r.y0;
+    a.y1 = r.y1;
+    a.f = view(io);
+    a.n_dy = full ? 0 : n_offs;
+    a.n_dx = a.n_dy;
+    a.dys_host = offs;
+    a.full_lo = -p->S;
+    a.full_hi = p->S;
+    a.evals = evals;
+    cudaError_t e;
+    {
+        ProfScope ps(P_REVGRID, s);
+        e = launch_revgrid(a, s);
+    }
+    return e == cudaSuccess ? QS_OK : cuda_fail(e, "revgrid launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *qs_last_error(void) { return g_err.c_str(); }
+
+const char *qs_version(void) { return "libqs 0.1 sm_100a (me_box two-phase, rank-chunked)"; }
+
+int qs_workspace_size(const qs_roi *roi, int32_t frame_w, int32_t frame_h, const qs_me_params *p, size_t *bytes) {
+    Roi r;
+    int rc = check_roi(roi, &r);
+    if (rc) return rc;
+    if (frame_w != r.W || frame_h != r.H) return fail(QS_EDIM, "frame size disagrees with roi");
+    if ((rc = check_params(p))) return rc;
+    if (!bytes) return fail(QS_EINVAL, "bytes is NULL");
+    size_t b = std::max(me_keys_bytes(r), rme_keys_bytes(r, p->S));
+    *bytes = (b + 255) & ~size_t(255);
+    return QS_OK;
+}
+
+int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, const void *ref, int64_t ref_pitch,
+                 const qs_roi *roi, const qs_me_params *p, const qs_checks *fuse, qs_field *out,
+                 unsigned long long *eval_count, void *workspace, size_t workspace_bytes, void *stream) {
+    Roi r;
+    int rc;
+    if ((rc = check_roi(roi, &r)) || (rc = check_params(p))) return rc;
+    const int esz = p->ref_type == QS_REF_F32 ? 4 : 1;
+    if ((rc = check_plane(cur, cur_pitch, r.W, "cur")) || (rc = check_plane(cur_mask, cur_pitch, r.W, "cur_mask")) ||
+        (rc = check_plane(ref, ref_pitch, (int64_t)r.W * esz, "ref")) || (rc = check_field(out, r.W, true)))
+        return rc;
+    const bool nnc = fuse && fuse->nnc, frmc = fuse && fuse->frmc;
+    if (fuse && nnc && fuse->nnc_threshold < 0) return fail(QS_EINVAL, "nnc_threshold < 0");
+    if (frmc && (rc = check_offsets(fuse->offsets, fuse->n_offsets, p->S))) return rc;
+    const int lo = nnc ? std::max(0, r.y0 - 2) : r.y0, hi = nnc ? std::min(r.H, r.y1 + 2) : r.y1;
+    const int K = p->K_h, KL = K / 2, KR = K - 1 - KL;
+    if ((rc = need_rows(r, lo, hi, "field")) || (rc = need_rows(r, lo - KL - p->S, hi + KR + p->S, "ME inputs")))
+        return rc;
+    const size_t need = me_keys_bytes(r);
+    if (!workspace || !aligned16(workspace) || workspace_bytes < need)
+        return fail(QS_EDIM, "workspace: need %zu bytes (16-byte aligned), got %zu", need, workspace_bytes);
+    const char *terr = nullptr;
+    const CandTables *t = cand_tables(p->S, &terr);
+    if (!t) return fail(QS_ECUDA, "%s", terr);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (r.y1 <= r.y0 || hi <= lo) return QS_OK;   // empty roi: nothing is written
+
+    auto *keys = static_cast<unsigned long long *>(workspace);
+    cudaError_t e = cudaMemsetAsync(keys, 0xff, sizeof(unsigned long long) * (size_t)(hi - lo) * r.W, s);
+    if (e != cudaSuccess) return cuda_fail(e, "memset keys");
+    BoxArgs a = box_args(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, t);
+    a.oy0 = lo;
+    a.oy1 = hi;
+    a.ox0 = 0;
+    a.ox1 = r.W;
+    a.tiles_x = (r.W + kTX - 1) / kTX;
+    a.tiles_y = (hi - lo + kTY - 1) / kTY;
+    a.keys = keys;
+    a.key_pitch = r.W;
+    {
+        ProfScope ps(P_ME_BOX, s);
+        e = launch_box(a, K, p->err == QS_SSD, false, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "me_box launch");
+
+    FinalizeArgs fa{};
+    fa.cur = a.cur;
+    fa.mask = a.mask;
+    fa.ref = a.ref;
+    fa.ref_f32 = a.ref_f32;
+    fa.ssd = p->err == QS_SSD;
+    fa.K = K;
+    fa.W = r.W;
+    fa.H = r.H;
+    fa.buf_y0 = r.b0;
+    fa.buf_rows = r.br;
+    fa.S = p->S;
+    fa.min_support = p->min_support;
+    fa.y0 = lo;
+    fa.y1 = hi;
+    fa.keys = keys;
+    fa.key_pitch = r.W;
+    fa.canon = t->canon;
+    fa.alpha = out->alpha;
+    fa.beta = out->beta;
+    fa.err = out->err;
+    fa.count = out->count;
+    fa.status = out->status;
+    fa.fpitch = out->pitch;
+    {
+        ProfScope ps(P_FINALIZE, s);
+        e = launch_finalize(fa, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "finalize launch");
+
+    if (nnc) {
+        {
+            ProfScope ps(P_NNC, s);
+            e = launch_nnc(view(out), r.W, r.H, r.b0, r.br, r.y0, r.y1, fuse->nnc_threshold, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "nnc launch");
+    }
+    if (frmc) {
+        if ((rc = run_frmc(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, fuse->offsets, fuse->n_offsets, 0, out,
+                           eval_count, s)))
+            return rc;
+    }
+    return QS_OK;
+}
+
+int qs_reverse_check(int32_t mode, const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, const void *ref,
+                     int64_t ref_pitch, const qs_roi *roi, const qs_me_params *p, qs_field *io,
+                     unsigned long long *eval_count, void *workspace, size_t workspace_bytes, void *stream) {
+    Roi r;
+    int rc;
+    if (mode != QS_RME && mode != QS_RMC) return fail(QS_EINVAL, "mode=%d", mode);
+    if ((rc = check_roi(roi, &r)) || (rc = check_params(p))) return rc;
+    const int esz = p->ref_type == QS_REF_F32 ? 4 : 1;
+    if ((rc = check_plane(cur, cur_pitch, r.W, "cur")) || (rc = check_plane(cur_mask, cur_pitch, r.W, "cur_mask")) ||
+        (rc = check_plane(ref, ref_pitch, (int64_t)r.W * esz, "ref")) || (rc = check_field(io, r.W, true)))
+        return rc;
+    const int K = p->K_h, KL = K / 2, KR = K - 1 - KL, S = p->S;
+    if ((rc = need_rows(r, r.y0, r.y1, "field"))) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const char *terr = nullptr;
+    const CandTables *t = cand_tables(S, &terr);
+    if (!t) return fail(QS_ECUDA, "%s", terr);
+    if (mode == QS_RMC) {
+        if ((rc = need_rows(r, r.y0 - S - KL, r.y1 + S + KR, "RMC inputs"))) return rc;
+        if (r.y1 <= r.y0) return QS_OK;
+        return run_frmc(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, nullptr, 0, 1, io, eval_count, s);
+    }
+    if ((rc = need_rows(r, r.y0 - 2 * S - KL, r.y1 + 2 * S + KR, "RME inputs"))) return rc;
+    const size_t need = rme_keys_bytes(r, S);
+    if (!workspace || !aligned16(workspace) || workspace_bytes < need)
+        return fail(QS_EDIM, "workspace: need %zu bytes (16-byte aligned), got %zu", need, workspace_bytes);
+    if (r.y1 <= r.y0) return QS_OK;
+    auto *keys = static_cast<unsigned long long *>(workspace);
+    cudaError_t e = cudaMemsetAsync(keys, 0xff, need, s);
+    if (e != cudaSuccess) return cuda_fail(e, "memset keys");
+    BoxArgs a = box_args(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, t);
+    a.oy0 = r.y0 - S;
+    a.oy1 = r.y1 + S;
+    a.ox0 = -S;
+    a.ox1 = r.W + S;
+    a.tiles_x = (r.W + 2 * S + kTX - 1) / kTX;
+    a.tiles_y = (r.y1 - r.y0 + 2 * S + kTY - 1) / kTY;
+    a.keys = keys;
+    a.key_pitch = r.W + 2 * S;
+    {
+        ProfScope ps(P_ME_BOX, s);
+        e = launch_box(a, K, p->err == QS_SSD, true, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "rme box launch");
+    RmeDecideArgs d{};
+    d.W = r.W;
+    d.H = r.H;
+    d.buf_y0 = r.b0;
+    d.buf_rows = r.br;
+    d.S = S;
+    d.y0 = r.y0;
+    d.y1 = r.y1;
+    d.f = view(io);
+    d.keys = keys;
+    d.key_pitch = r.W + 2 * S;
+    d.canon = t->canon;
+    d.evals = eval_count;
+    d.n_cand = t->n;
+    {
+        ProfScope ps(P_RME_DECIDE, s);
+        e = launch_rme_decide(d, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "rme decide launch");
+    return QS_OK;
+}
+
+int qs_frmc(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, const void *ref, int64_t ref_pitch,
+            const qs_roi *roi, const qs_me_params *p, const int8_t *offsets, int32_t n_offsets, qs_field *io,
+            unsigned long long *eval_count, void *stream) {
+    Roi r;
+    int rc;
+    if ((rc = check_roi(roi, &r)) || (rc = check_params(p))) return rc;
+    const int esz = p->ref_type == QS_REF_F32 ? 4 : 1;
+    if ((rc = check_plane(cur, cur_pitch, r.W, "cur")) || (rc = check_plane(cur_mask, cur_pitch, r.W, "cur_mask")) ||
+        (rc = check_plane(ref, ref_pitch, (int64_t)r.W * esz, "ref")) || (rc = check_field(io, r.W, true)))
+        return rc;
+    if ((rc = check_offsets(offsets, n_offsets, p->S))) return rc;
+    const int K = p->K_h, KL = K / 2, KR = K - 1 - KL;
+    if ((rc = need_rows(r, r.y0, r.y1, "field")) || (rc = need_rows(r, r.y0 - p->S - KL, r.y1 + p->S + KR, "FRMC inputs")))
+        return rc;
+    if (r.y1 <= r.y0) return QS_OK;
+    return run_frmc(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, offsets, n_offsets, 0, io, eval_count,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int qs_nnc(qs_field *io, const qs_roi *roi, int32_t threshold, void *stream) {
+    Roi r;
+    int rc;
+    if ((rc = check_roi(roi, &r))) return rc;
+    if ((rc = check_field(io, r.W, false))) return rc;
+    if (threshold < 0) return fail(QS_EINVAL, "threshold < 0");
+    if ((rc = need_rows(r, r.y0 - 2, r.y1 + 2, "NNC field"))) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    {
+        ProfScope ps(P_NNC, s);
+        e = launch_nnc(view(io), r.W, r.H, r.b0, r.br, r.y0, r.y1, threshold, s);
+    }
+    return e == cudaSuccess ? QS_OK : cuda_fail(e, "nnc launch");
+}
+
+int qs_project(const qs_field *f, const uint8_t *past_val, const uint8_t *past_mask, int64_t past_pitch,
+               const qs_roi *roi, uint32_t *sum, uint8_t *cnt, int64_t acc_pitch, void *stream) {
+    Roi r;
+    int rc;
+    if ((rc = check_roi(roi, &r))) return rc;
+    if ((rc = check_field(f, r.W, false))) return rc;
+    if ((rc = check_plane(past_val, past_pitch, r.W, "past_val")) ||
+        (rc = check_plane(past_mask, past_pitch, r.W, "past_mask")))
+        return rc;
+    if (!sum || !cnt) return fail(QS_EINVAL, "sum/cnt is NULL");
+    if (acc_pitch < r.W) return fail(QS_EDIM, "acc_pitch < width");
+    if ((reinterpret_cast<uintptr_t>(sum) & 3)) return fail(QS_EALIGN, "sum not 4-byte aligned");
+    if ((rc = need_rows(r, r.y0, r.y1, "field"))) return rc;
+    ProjectArgs a{};
+    a.f = FieldView{f->alpha, f->beta, f->err, f->count, f->status, f->pitch};
+    a.past_val = Plane{past_val, past_pitch};
+    a.past_mask = Plane{past_mask, past_pitch};
+    a.W = r.W;
+    a.H = r.H;
+    a.buf_y0 = r.b0;
+    a.buf_rows = r.br;
+    a.y0 = r.y0;
+    a.y1 = r.y1;
+    a.sum = sum;
+    a.cnt = cnt;
+    a.acc_pitch = acc_pitch;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    {
+        ProfScope ps(P_PROJECT, s);
+        e = launch_project(a, s);
+    }
+    return e == cudaSuccess ? QS_OK : cuda_fail(e, "project launch");
+}
+
+int qs_profile_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on != 0;
+    return QS_OK;
+}
+
+int qs_profile_read(const char *kernel, double *total_ms, int64_t *launches) {
+    if (!kernel || !total_ms || !launches) return fail(QS_EINVAL, "NULL argument");
+    int want = -2;
+    if (!strcmp(kernel, "*")) want = -1;
+    for (int k = 0; k < P_COUNT; ++k)
+        if (!strcmp(kernel, kProfNames[k])) want = k;
+    if (want == -2) return fail(QS_EINVAL, "unknown kernel '%s'", kernel);
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    double t = 0.0;
+    int64_t n = 0;
+    for (const ProfRec &r : g_prof.recs) {
+        if (want >= 0 && r.kernel != want) continue;
+        if (cudaEventSynchronize(r.stop) != cudaSuccess) return cuda_fail(cudaGetLastError(), "event sync");
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.start, r.stop) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "event elapsed");
+        t += ms;
+        ++n;
+    }
+    *total_ms = t;
+    *launches = n;
+    return QS_OK;
+}
+
+int qs_profile_reset(void) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (const ProfRec &r : g_prof.recs) {
+        cudaEventSynchronize(r.stop);
+        g_prof.pool.push_back(r.start);
+        g_prof.pool.push_back(r.stop);
+    }
+    g_prof.recs.clear();
+    return QS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// qs_internal.cuh -- internal declarations of libqs (the CUDA product path).
+// Shares nothing with oracle/ (test infrastructure).  See include/qs.h for the
+// ABI and DESIGN.md for the kernels, their rooflines and the readings R1-R26.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/qs.h"
+
+namespace qs {
+
+// Status codes mirror include/qs.h (PAPER.md:68-115 path; R4, R6, R16).
+constexpr uint8_t kNotTarget = QS_NOT_TARGET;
+constexpr uint8_t kInvalid = QS_INVALID;
+constexpr uint8_t kCandidate = QS_CANDIDATE;
+constexpr uint8_t kAccepted = QS_ACCEPTED;
+constexpr uint8_t kRejected = QS_REJECTED;
+
+// ME box-kernel tiling.
+constexpr int kTX = 64;        // output columns per CTA tile
+constexpr int kTY = 56;        // output rows per CTA tile (TY + K - 1 <= 64 for K <= 9)
+constexpr int kNT = 256;       // threads per CTA
+constexpr int kRun = 16;       // phase A: H columns per thread
+constexpr int kSeg = 14;       // phase B: output rows per thread (4 segments x 14 = 56)
+constexpr int kTXP = 68;       // padded row pitch (floats) of the H planes in smem
+constexpr int kChunkRows = 7;  // alpha rows of candidates per work unit
+
+// One device-resident candidate table per (device, S).
+struct CandTables {
+    int S = -1;
+    int n = 0;                       // (2S+1)^2
+    int n_chunks = 0;
+    int32_t *canon = nullptr;        // [n]   rank -> (alpha & 0xff) | (beta & 0xff) << 8
+    int32_t *chunked = nullptr;      // [n]   chunk-major, rank order inside a chunk:
+                                     //       (alpha & 0xff) | (beta & 0xff) << 8 | rank << 16
+    int32_t *chunk_off = nullptr;    // [n_chunks + 1]
+};
+
+// Returns tables for S on the current device (built once; thread-safe).
+const CandTables *cand_tables(int S, const char **err);
+
+// Geometry of a plane window: global row y lives at base + (y - buf_y0) * pitch.
+struct Plane {
+    const uint8_t *p;   // base of buffer row 0
+    int64_t pitch;      // bytes
+};
+
+// Arguments of the box kernels (forward ME and dense reverse ME).
+struct BoxArgs {
+    Plane cur, mask, ref;
+    int ref_f32;
+    int W, H, buf_y0, buf_rows;
+    int S, min_support;
+    int oy0, oy1, ox0, ox1;          // output domain (rows / cols, frame coords; may exceed the frame for REV)
+    int tiles_x, tiles_y, n_chunks;
+    const int32_t *chunked;
+    const int32_t *chunk_off;
+    unsigned long long *keys;        // [oy1-oy0][key_pitch]
+    int64_t key_pitch;
+};
+
+// Launchers (me_box.cu).  Return cudaError_t of the launch.
+cudaError_t launch_box(const BoxArgs &a, int K, bool ssd, bool reverse, cudaStream_t s);
+
+struct FinalizeArgs {
+    Plane cur, mask, ref;
+    int ref_f32, ssd, K;
+    int W, H, buf_y0, buf_rows;
+    int S, min_support;
+    int y0, y1;                      // rows to finalize
+    const unsigned long long *keys;  // keys row 0 == global row y0
+    int64_t key_pitch;
+    const int32_t *canon;
+    int8_t *alpha, *beta;
+    void *err;
+    uint8_t *count, *status;
+    int64_t fpitch;                  // field pitch (elements); field row 0 == global buf_y0
+};
+cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s);
+
+// Checks (checks.cu).
+struct FieldView {
+    int8_t *alpha, *beta;
+    void *err;
+    uint8_t *count, *status;
+    int64_t pitch;                   // elements; row 0 == global buf_y0
+};
+
+cudaError_t launch_nnc(FieldView f, int W, int H, int buf_y0, int buf_rows, int y0, int y1, int threshold,
+                       cudaStream_t s);
+
+struct RevGridArgs {
+    Plane cur, mask, ref;
+    int ref_f32, ssd, K;
+    int W, H, buf_y0, buf_rows;
+    int min_support;
+    int y0, y1;
+    FieldView f;
+    int n_dy, n_dx;                  // delta grid = dys x dxs
+    const int8_t *dys_host;          // copied into kernel params (<= 15 entries) or full range
+    int full_lo, full_hi;            // if n_dy == 0: delta in [full_lo, full_hi]^2 (RMC)
+    unsigned long long *evals;
+};
+cudaError_t launch_revgrid(const RevGridArgs &a, cudaStream_t s);
+
+struct RmeDecideArgs {
+    int W, H, buf_y0, buf_rows, S;
+    int y0, y1;
+    FieldView f;
+    const unsigned long long *keys;  // reverse keys over x rows [y0-S, y1+S), cols [-S, W+S)
+    int64_t key_pitch;
+    const int32_t *canon;
+    unsigned long long *evals;
+    int n_cand;
+};
+cudaError_t launch_rme_decide(const RmeDecideArgs &a, cudaStream_t s);
+
+struct ProjectArgs {
+    FieldView f;
+    Plane past_val, past_mask;
+    int W, H, buf_y0, buf_rows, y0, y1;
+    uint32_t *sum;
+    uint8_t *cnt;
+    int64_t acc_pitch;
+};
+cudaError_t launch_project(const ProjectArgs &a, cudaStream_t s);
+
+}  // namespace qs

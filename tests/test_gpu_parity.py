@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar: uint8 references -> every plane bit-exact (alpha, beta, err, count,
+status, PR sum/cnt, evaluation counts).  float32 references -> statuses equal, vectors equal
+except documented near-ties, err within 1e-5 relative (north_star).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from gpu_helpers import (assert_field_equal, f32_me_compare, gpu_check, gpu_me, gpu_project)
+    import paper_2203_09200_b200 as qs
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+# ---------------------------------------------------------------------------
+# Config 1: the correctness config, every pair, whole chain (ME -> NNC -> FRMC -> PR)
+# ---------------------------------------------------------------------------
+def test_config1_full_chain_bit_exact():
+    seq = synth.make_sequence(1)
+    for t in (1, 2):
+        osum = np.zeros((64, 64), np.uint32)
+        ocnt = np.zeros((64, 64), np.uint8)
+        gacc = (np.zeros((64, 64), np.uint32), np.zeros((64, 64), np.uint8))
+        for d in range(1, min(3, t) + 1):
+            inp = synth.pair_inputs(seq, t, d)
+            g, gev = gpu_me(inp, K=8, S=8, fuse=qs.make_checks())
+            o, oev = oracle.pair_chain(inp, K=8, S=8, check="nnc_frmc")
+            assert_field_equal(g, o, what=f"t={t} d={d}")
+            assert gev == oev
+            osum, ocnt = oracle.project(o, inp["past_val"], inp["past_mask"], osum, ocnt)
+            gacc = gpu_project(inp, g, gacc)
+        assert np.array_equal(gacc[0], osum) and np.array_equal(gacc[1], ocnt)
+
+
+def test_config2_me_and_cascade_bit_exact():
+    seq = synth.make_sequence(2)
+    for (t, d) in ((5, 1), (6, 3)):
+        inp = synth.pair_inputs(seq, t, d)
+        g, gev = gpu_me(inp, K=8, S=16, fuse=qs.make_checks())
+        o, oev = oracle.pair_chain(inp, K=8, S=16, check="nnc_frmc")
+        assert_field_equal(g, o, what=f"c2 t={t} d={d}")
+        assert gev == oev
+
+
+# ---------------------------------------------------------------------------
+# Fuzz: random small instances, every K the build supports, S from 0, SAD/SSD, ragged sizes
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_me_u8(seed):
+    rng = np.random.default_rng(seed)
+    K = int(rng.integers(1, 10))
+    S = int(rng.integers(0, 7))
+    W = int(rng.integers(1, 50)) * 2
+    H = int(rng.integers(1, 40)) * 2
+    ssd = bool(rng.integers(0, 2))
+    ms = int(rng.integers(1, 12))
+    inp = synth.rank_free_random_instance(100 + seed, W, H, smooth=bool(seed % 2), dynamic=bool(seed % 3), t=seed)
+    g, _ = gpu_me(inp, K=K, S=S, min_support=ms, ssd=ssd)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=K, S=S, min_support=ms, ssd=ssd)
+    assert_field_equal(g, o, what=f"seed={seed} K={K} S={S} {W}x{H} ssd={ssd} ms={ms}")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_checks_u8_staged(seed):
+    """Each check on the same (oracle) field: statuses and counts bit-exact."""
+    rng = np.random.default_rng(1000 + seed)
+    K = int(rng.choice([3, 4, 8, 9]))
+    S = int(rng.integers(1, 6))
+    ssd = bool(seed % 2)
+    W, H = 40, 30
+    inp = synth.rank_free_random_instance(300 + seed, W, H, smooth=True)
+    kw = dict(K=K, S=S, min_support=4, ssd=ssd)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], **kw)
+    offs = tuple(x for x in (-3, -1, 0, 1, 3) if abs(x) <= S)
+    st, ev = gpu_check("frmc", inp, o, offsets=offs, **kw)
+    ost, oev = oracle.frmc(inp["cur"], inp["cur_mask"], inp["ref"], o, offsets=offs, **kw)
+    assert np.array_equal(st, ost) and ev == oev
+    st, ev = gpu_check("rmc", inp, o, **kw)
+    ost, oev = oracle.rmc(inp["cur"], inp["cur_mask"], inp["ref"], o, **kw)
+    assert np.array_equal(st, ost) and ev == oev
+    st, ev = gpu_check("rme", inp, o, **kw)
+    ost, oev = oracle.rme(inp["cur"], inp["cur_mask"], inp["ref"], o, **kw)
+    assert np.array_equal(st, ost) and ev == oev
+    st, _ = gpu_check("nnc", inp, o)
+    assert np.array_equal(st, oracle.nnc(o))
+
+
+def test_nnc_golden_on_gpu(golden):
+    g = golden("nnc_hand.json")
+    for case in g["cases"]:
+        a = np.array(case["alpha"], np.int8)
+        H, W = a.shape
+        if W % 2 or H % 2:   # the ABI requires even frames; pad with NOT_TARGET entries
+            Hp, Wp = H + H % 2, W + W % 2
+        else:
+            Hp, Wp = H, W
+        fld = {k: np.zeros((Hp, Wp), dt) for k, dt in (("alpha", np.int8), ("beta", np.int8), ("err", np.uint32),
+                                                        ("count", np.uint8), ("status", np.uint8))}
+        fld["alpha"][:H, :W] = a
+        fld["beta"][:H, :W] = np.array(case["beta"], np.int8)
+        fld["status"][:H, :W] = np.array(case["status"], np.uint8)
+        inp = dict(cur=np.zeros((Hp, Wp), np.uint8), cur_mask=np.zeros((Hp, Wp), np.uint8),
+                   ref=np.zeros((Hp, Wp), np.uint8), past_val=np.zeros((Hp, Wp), np.uint8),
+                   past_mask=np.zeros((Hp, Wp), np.uint8))
+        st, _ = gpu_check("nnc", inp, fld)
+        assert np.array_equal(st[:H, :W], np.array(case["expect"], np.uint8)), case["name"]
+
+
+def test_project_golden_on_gpu(golden):
+    g = golden("project_hand.json")
+    acc = (np.zeros((4, 4), np.uint32), np.zeros((4, 4), np.uint8))
+    for r in g["refs"]:
+        fld = dict(alpha=np.array(r["alpha"], np.int8), beta=np.array(r["beta"], np.int8),
+                   err=np.zeros((4, 4), np.uint32), count=np.zeros((4, 4), np.uint8),
+                   status=np.array(r["status"], np.uint8))
+        inp = dict(cur=np.zeros((4, 4), np.uint8), cur_mask=np.zeros((4, 4), np.uint8), ref=np.zeros((4, 4), np.uint8),
+                   past_val=np.array(r["past_val"], np.uint8), past_mask=np.array(g["past_mask"], np.uint8))
+        acc = gpu_project(inp, fld, acc)
+    assert np.array_equal(acc[0], np.array(g["expect_sum"])) and np.array_equal(acc[1], np.array(g["expect_cnt"]))
+
+
+def test_p13_micro_golden_on_gpu(golden):
+    g = golden("p13_micro.json")
+    inp = dict(cur=np.array(g["cur"], np.uint8), cur_mask=np.array(g["mask"], np.uint8),
+               ref=np.array(g["ref"], np.uint8))
+    f, _ = gpu_me(inp, K=g["K"], S=g["S"], min_support=g["min_support"])
+    for ex in g["expect"]:
+        y, x = ex["p"]
+        assert (int(f["alpha"][y, x]), int(f["beta"][y, x])) == tuple(ex["v"])
+        assert int(f["err"][y, x]) == ex["e"] and int(f["count"][y, x]) == ex["n"]
+
+
+# ---------------------------------------------------------------------------
+# Float-reference path (config 4's arithmetic)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("S,K,ssd", [(24, 8, False), (6, 8, True), (5, 3, False), (4, 9, False)])
+def test_f32_me_tolerance(S, K, ssd):
+    seq = synth.make_sequence(4, w=160, h=112)
+    inp = synth.pair_inputs(seq, 7, 2)
+    assert inp["ref"].dtype == np.float32
+    g, _ = gpu_me(inp, K=K, S=S, ssd=ssd)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=K, S=S, ssd=ssd)
+    ties = f32_me_compare(g, o, inp, K, S, ssd=ssd)
+    assert len(ties) <= max(3, int(1e-3 * (o["status"] == oracle.CANDIDATE).sum())), ties
+
+
+def test_f32_checks_bit_exact_given_field():
+    """FRMC / RMC re-sum each reverse cost in the oracle's row-major fp32 order: decisions equal."""
+    seq = synth.make_sequence(4, w=96, h=64)
+    inp = synth.pair_inputs(seq, 9, 1)
+    kw = dict(K=8, S=8)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], **kw)
+    st, ev = gpu_check("frmc", inp, o, **kw)
+    ost, oev = oracle.frmc(inp["cur"], inp["cur_mask"], inp["ref"], o, **kw)
+    assert np.array_equal(st, ost) and ev == oev
+    st, ev = gpu_check("rmc", inp, o, **kw)
+    ost, oev = oracle.rmc(inp["cur"], inp["cur_mask"], inp["ref"], o, **kw)
+    assert np.array_equal(st, ost) and ev == oev
+    st, ev = gpu_check("rme", inp, o, **kw)
+    ost, oev = oracle.rme(inp["cur"], inp["cur_mask"], inp["ref"], o, **kw)
+    diff = st != ost
+    assert ev == oev and diff.sum() <= max(2, int(1e-3 * (o["status"] == oracle.CANDIDATE).sum()))
+
+
+# ---------------------------------------------------------------------------
+# Full-size configs in the bench's launch configuration, sampled rows
+# ---------------------------------------------------------------------------
+def _sampled_rows(H, S, rng, n_mid=2):
+    rows = [(0, 2), (H - 2, H)]
+    for _ in range(n_mid):
+        y = int(rng.integers(S + 8, H - S - 8))
+        rows.append((y, y + 1))
+    return rows
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_fullsize_u8_sampled(cfg):
+    c = synth.CONFIGS[cfg]
+    seq = synth.make_sequence(cfg)
+    inp = synth.pair_inputs(seq, 3, 1)
+    g, _ = gpu_me(inp, K=8, S=c.S, fuse=qs.make_checks())
+    rng = np.random.default_rng(cfg)
+    for rows in _sampled_rows(c.h, c.S, rng):
+        o, _ = oracle.pair_chain(inp, K=8, S=c.S, check="nnc_frmc", rows=rows)
+        assert_field_equal(g, o, rows=rows, what=f"config {cfg} rows {rows}")
+
+
+def test_fullsize_config4_f32_sampled():
+    c = synth.CONFIGS[4]
+    seq = synth.make_sequence(4)
+    inp = synth.pair_inputs(seq, 4, 3)
+    g, _ = gpu_me(inp, K=8, S=c.S)
+    rng = np.random.default_rng(4)
+    for rows in _sampled_rows(c.h, c.S, rng, n_mid=2):
+        o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=8, S=c.S, rows=rows)
+        f32_me_compare(g, o, inp, 8, c.S, rows=rows)
+
+
+# ---------------------------------------------------------------------------
+# Edge cases
+# ---------------------------------------------------------------------------
+def test_empty_roi_writes_nothing():
+    inp = synth.rank_free_random_instance(5, 32, 32)
+    g, ev = gpu_me(inp, K=8, S=4, rows=(10, 10), fuse=qs.make_checks(offsets=(-1, 0, 1)))
+    assert ev == 0 and np.all(g["status"] == 0)
+
+
+def test_tiny_frame_and_all_invalid():
+    inp = synth.rank_free_random_instance(6, 2, 2)
+    g, _ = gpu_me(inp, K=8, S=2)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=8, S=2)
+    assert_field_equal(g, o)
+    inp = synth.rank_free_random_instance(7, 20, 18)
+    g, _ = gpu_me(inp, K=8, S=3, min_support=26)
+    assert np.all(g["status"][inp["cur_mask"] == 0] == oracle.INVALID)
+
+
+def test_row_bands_equal_full_frame():
+    """Fake multi-rank: each band computed with buffers holding only band + halo rows (R25)."""
+    seq = synth.make_sequence(2)
+    inp = synth.pair_inputs(seq, 8, 2)
+    H, W = inp["cur"].shape
+    S, K = 16, 8
+    full, fev = gpu_me(inp, K=K, S=S, fuse=qs.make_checks())
+    G = 3
+    bounds = [2 * ((r * H) // (2 * G)) for r in range(G + 1)]
+    halo = S + K + 2
+    out = {k: np.zeros_like(v) for k, v in full.items()}
+    tot = 0
+    for r in range(G):
+        y0, y1 = bounds[r], bounds[r + 1]
+        b0, b1 = max(0, y0 - halo), min(H, y1 + halo)
+        g, ev = gpu_me(inp, K=K, S=S, fuse=qs.make_checks(), rows=(y0, y1), band=(b0, b1 - b0))
+        tot += ev
+        for k in out:
+            out[k][y0:y1] = g[k][y0:y1]
+    assert_field_equal(out, full, what="bands vs full")
+    assert tot == fev
+
+
+def test_abi_errors_on_device():
+    inp = synth.rank_free_random_instance(8, 16, 16)
+    p = {k: qs.to_plane(inp[k]) for k in ("cur", "cur_mask", "ref")}
+    f = qs.Field.alloc(16, 16, False)
+    roi = qs.make_roi(16, 16)
+    with pytest.raises(qs.QsError) as e:
+        qs.qs_me_search(p["cur"], p["cur_mask"], p["ref"], roi, qs.make_params(K=10, S=2), f)
+    assert e.value.code == qs.QS_EINVAL
+    with pytest.raises(qs.QsError) as e:
+        qs.qs_me_search(p["cur"], p["cur_mask"], p["ref"], qs.make_roi(16, 16, 0, 16, 4, 12),
+                        qs.make_params(K=8, S=2), f)
+    assert e.value.code == qs.QS_EDIM
+    with pytest.raises(qs.QsError) as e:
+        qs.qs_frmc(p["cur"], p["cur_mask"], p["ref"], roi, qs.make_params(K=8, S=2), f, offsets=(-1, 1))
+    assert e.value.code == qs.QS_EINVAL
+
+
+def test_deterministic_repeat():
+    seq = synth.make_sequence(2)
+    inp = synth.pair_inputs(seq, 9, 1)
+    a, ea = gpu_me(inp, K=8, S=16, fuse=qs.make_checks())
+    b, eb = gpu_me(inp, K=8, S=16, fuse=qs.make_checks())
+    assert_field_equal(a, b) and ea == eb

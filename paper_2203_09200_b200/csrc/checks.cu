@@ -183,6 +183,212 @@ __global__ void revgrid_kernel(RevGridArgs a, DeltaSet ds) {
 }
 
 // ---------------------------------------------------------------------------
+// Tiled reverse-cost grid for K = 8 (the configs' template).  One CTA = a 16x16
+// tile of field entries.  The reference region the entries' x = p+v windows can
+// reach and the current-frame region the shifted windows p+delta+o can reach are
+// staged once into shared memory (float, NaN = no term), with the current mask
+// as bit rows.  Work items are (entry, delta_y, delta_x-group of up to 7); an item
+// keeps 7 accumulators and walks the 8 template rows: per row it loads the 8
+// reference values of the x window and the 22-wide current segment, and adds
+// phi(ref - cur) for every (delta_x, o_x) from registers with static indices.
+// Each reverse cost is still summed in row-major o order (R23), so decisions
+// equal the oracle's; the support n' comes from popcounts of the mask bits.
+// Delta_x patterns: PAT 0 = the paper's {-7,-3,-1,0,1,3,7},
+// PAT 1 = 7 consecutive values (RMC's [-S, S] in groups).
+// ---------------------------------------------------------------------------
+constexpr int kFT = 16;          // tile edge (entries)
+constexpr int kFK = 8;           // template
+constexpr int kFSeg = kFK + 14;  // current-row segment per item (22)
+
+template <int PAT>
+__device__ __forceinline__ constexpr int pat_j(int k) {
+    // column of delta_x within the 15-wide group span (delta_x - dx0)
+    return PAT == 0 ? (k == 0 ? 0 : k == 1 ? 4 : k == 2 ? 6 : k == 3 ? 7 : k == 4 ? 8 : k == 5 ? 10 : 14) : k;
+}
+
+struct TileGridArgs {
+    RevGridArgs a;
+    int n_dy;          // delta_y values
+    int8_t dys[16];    // PAT 0: the offsets; PAT 1: unused (dy = lo + i)
+    int lo;            // PAT 1: first delta (== -S)
+    int n_groups;      // delta_x groups
+    int n_last;        // deltas in the last group (PAT 1)
+    int maxd;          // max |delta|
+    int S;             // max |v|
+    int n_total;       // |delta set| for the evaluation counter
+};
+
+template <int PAT, bool SSD, bool F32>
+__global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g) {
+    extern __shared__ __align__(16) float sm[];
+    const RevGridArgs &a = g.a;
+    constexpr int KL = kFK / 2;
+    const int tx0 = blockIdx.x * kFT, ty0 = a.y0 + blockIdx.y * kFT;
+    // Regions (global coords of their row/col 0) and sizes.
+    const int cy0 = ty0 - g.maxd - KL, cx0 = tx0 - g.maxd - KL;
+    const int CR = kFT + 2 * g.maxd + kFK - 1, CC = CR;
+    const int ry0 = ty0 - g.S - KL, rx0 = tx0 - g.S - KL;
+    const int RR = kFT + 2 * g.S + kFK - 1, RC = RR;
+    const int cpitch = CC + 16 + 1;          // room for a 22-wide read past the region edge
+    const int rpitch = RC + 1;
+    const int mwords = (CC + 16 + 31) / 32 + 1;
+    float *Cs = sm;
+    float *Rs = Cs + CR * cpitch;
+    uint32_t *Mb = reinterpret_cast<uint32_t *>(Rs + RR * rpitch);
+    int *ent = reinterpret_cast<int *>(Mb + CR * mwords);   // packed entries [256]
+    float *ent_m0 = reinterpret_cast<float *>(ent + kFT * kFT);
+    uint32_t *ent_e0 = reinterpret_cast<uint32_t *>(ent_m0 + kFT * kFT);
+    uint8_t *rej = reinterpret_cast<uint8_t *>(ent_e0 + kFT * kFT);
+    __shared__ int n_ent;
+    const int tid = threadIdx.x;
+    if (tid == 0) n_ent = 0;
+    for (int i = tid; i < CR * mwords; i += blockDim.x) Mb[i] = 0u;
+    __syncthreads();
+    // Stage the current region (NaN where unmeasured / outside) and its mask bits.
+    for (int i = tid; i < CR * cpitch; i += blockDim.x) {
+        const int r = i / cpitch, c = i - r * cpitch;
+        const int gy = cy0 + r, gx = cx0 + c;
+        float v = __int_as_float(0x7fc00000);
+        if (c < CC && gy >= 0 && gy < a.H && gx >= 0 && gx < a.W && gy >= a.buf_y0 && gy < a.buf_y0 + a.buf_rows) {
+            const int64_t rr = gy - a.buf_y0;
+            if (a.mask.p[rr * a.mask.pitch + gx]) {
+                v = (float)a.cur.p[rr * a.cur.pitch + gx];
+                atomicOr(&Mb[r * mwords + (c >> 5)], 1u << (c & 31));
+            }
+        }
+        Cs[i] = v;
+    }
+    // Stage the reference region (NaN outside the frame / buffer).
+    for (int i = tid; i < RR * rpitch; i += blockDim.x) {
+        const int r = i / rpitch, c = i - r * rpitch;
+        const int gy = ry0 + r, gx = rx0 + c;
+        float v = __int_as_float(0x7fc00000);
+        if (c < RC && gy >= 0 && gy < a.H && gx >= 0 && gx < a.W && gy >= a.buf_y0 && gy < a.buf_y0 + a.buf_rows) {
+            const int64_t rr = gy - a.buf_y0;
+            v = F32 ? reinterpret_cast<const float *>(a.ref.p + rr * a.ref.pitch)[gx] : (float)a.ref.p[rr * a.ref.pitch + gx];
+        }
+        Rs[i] = v;
+    }
+    // Checkable entries of the tile.
+    {
+        const int ly = tid / kFT, lx = tid % kFT;
+        const int gy = ty0 + ly, gx = tx0 + lx;
+        if (gy < a.y1 && gx < a.W) {
+            const int64_t fi = (int64_t)(gy - a.buf_y0) * a.f.pitch + gx;
+            if (checkable(a.f.status[fi])) {
+                const int slot = atomicAdd(&n_ent, 1);
+                const int va = a.f.alpha[fi], vb = a.f.beta[fi];
+                ent[slot] = (ly) | (lx << 8) | ((va & 0xff) << 16) | ((vb & 0xff) << 24);
+                const int n0 = a.f.count[fi];
+                if (F32) {
+                    ent_m0[slot] = __fdiv_rn(reinterpret_cast<const float *>(a.f.err)[fi], (float)n0);
+                    ent_e0[slot] = (uint32_t)n0;
+                } else {
+                    ent_e0[slot] = reinterpret_cast<const uint32_t *>(a.f.err)[fi];
+                    ent_m0[slot] = __int_as_float(n0);
+                }
+                rej[slot] = 0;
+            }
+        }
+    }
+    __syncthreads();
+    const int ne = n_ent;
+    const int per_entry = g.n_dy * g.n_groups;
+    const int items = ne * per_entry;
+    for (int it = tid; it < items; it += blockDim.x) {
+        const int e = it / per_entry;
+        if (rej[e]) continue;                            // decision already made ("reject iff any")
+        const int rem = it - e * per_entry;
+        const int iy = rem / g.n_groups, grp = rem - iy * g.n_groups;
+        const int pk = ent[e];
+        const int ly = pk & 0xff, lx = (pk >> 8) & 0xff;
+        const int va = (int)(int8_t)((pk >> 16) & 0xff), vb = (int)(int8_t)((pk >> 24) & 0xff);
+        const int dy = PAT == 0 ? g.dys[iy] : g.lo + iy;
+        const int dx0 = PAT == 0 ? -7 : g.lo + 7 * grp;
+        const int nk = PAT == 0 ? 7 : (grp == g.n_groups - 1 ? g.n_last : 7);
+        float acc[7];
+        int cnt[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) { acc[k] = 0.f; cnt[k] = 0; }
+        // Region coordinates of row 0 / col 0 of the windows.
+        const int crow = (ty0 + ly + dy - KL) - cy0, ccol = (tx0 + lx + dx0 - KL) - cx0;
+        const int rrow = (ty0 + ly + va - KL) - ry0, rcol = (tx0 + lx + vb - KL) - rx0;
+#pragma unroll 1
+        for (int oy = 0; oy < kFK; ++oy) {
+            const float *cp = Cs + (crow + oy) * cpitch + ccol;
+            const float *rp = Rs + (rrow + oy) * rpitch + rcol;
+            float c[kFSeg], r[kFK];
+#pragma unroll
+            for (int j = 0; j < kFSeg; ++j) c[j] = cp[j];
+            uint32_t rb = 0;
+#pragma unroll
+            for (int j = 0; j < kFK; ++j) {
+                r[j] = rp[j];
+                rb |= (r[j] == r[j]) ? (1u << j) : 0u;
+            }
+            const uint32_t *mw = Mb + (crow + oy) * mwords;
+            const int bo = ccol;
+            const uint32_t bits = __funnelshift_r(mw[bo >> 5], mw[(bo >> 5) + 1], bo & 31);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const int j = pat_j<PAT>(k);
+#pragma unroll
+                for (int ox = 0; ox < kFK; ++ox) {
+                    const float d = r[ox] - c[ox + j];
+                    const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
+                    acc[k] = __fadd_rn(acc[k], fmaxf(t, 0.f));     // NaN (no term) -> +0: exact no-op
+                }
+                cnt[k] += __popc((bits >> j) & rb);
+            }
+        }
+        bool reject = false;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            if (k >= nk) continue;
+            const int dx = dx0 + pat_j<PAT>(k);
+            if (dy == 0 && dx == 0) continue;
+            if (cnt[k] < a.min_support) continue;             // SENTINEL never rejects (R11)
+            if (F32) {
+                if (__fdiv_rn(acc[k], (float)cnt[k]) < ent_m0[e]) reject = true;
+            } else {
+                const unsigned long long ek = (unsigned long long)acc[k];
+                const unsigned n0 = (unsigned)__float_as_int(ent_m0[e]);
+                if (ek * n0 < (unsigned long long)ent_e0[e] * (unsigned)cnt[k]) reject = true;
+            }
+        }
+        if (reject) rej[e] = 1;
+    }
+    __syncthreads();
+    for (int e = tid; e < ne; e += blockDim.x) {
+        const int pk = ent[e];
+        const int gy = ty0 + (pk & 0xff), gx = tx0 + ((pk >> 8) & 0xff);
+        a.f.status[(int64_t)(gy - a.buf_y0) * a.f.pitch + gx] = rej[e] ? kRejected : kAccepted;
+    }
+    if (a.evals && tid == 0 && ne) atomicAdd(a.evals, (unsigned long long)ne * (unsigned long long)g.n_total);
+}
+
+template <int PAT, bool SSD, bool F32>
+cudaError_t launch_tile_t(const TileGridArgs &g, cudaStream_t s) {
+    const int CR = kFT + 2 * g.maxd + kFK - 1, CC = CR;
+    const int RR = kFT + 2 * g.S + kFK - 1, RC = RR;
+    const int cpitch = CC + 16 + 1, rpitch = RC + 1, mwords = (CC + 16 + 31) / 32 + 1;
+    const size_t smem = sizeof(float) * ((size_t)CR * cpitch + (size_t)RR * rpitch) + sizeof(uint32_t) * CR * mwords +
+                        (sizeof(int) + sizeof(float) + sizeof(uint32_t) + 1) * kFT * kFT + 16;
+    auto fn = revgrid_tile_kernel<PAT, SSD, F32>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grd((g.a.W + kFT - 1) / kFT, (g.a.y1 - g.a.y0 + kFT - 1) / kFT);
+    fn<<<grd, 256, smem, s>>>(g);
+    return cudaGetLastError();
+}
+
+template <int PAT>
+cudaError_t launch_tile_p(const TileGridArgs &g, cudaStream_t s) {
+    if (g.a.ref_f32) return g.a.ssd ? launch_tile_t<PAT, true, true>(g, s) : launch_tile_t<PAT, false, true>(g, s);
+    return g.a.ssd ? launch_tile_t<PAT, true, false>(g, s) : launch_tile_t<PAT, false, false>(g, s);
+}
+
+// ---------------------------------------------------------------------------
 // RME decision from the dense reverse keys (argmin over u in rank order).
 // ---------------------------------------------------------------------------
 __global__ void rme_decide_kernel(RmeDecideArgs a) {
@@ -245,6 +451,42 @@ cudaError_t launch_nnc(FieldView f, int W, int H, int buf_y0, int buf_rows, int 
 
 cudaError_t launch_revgrid(const RevGridArgs &a, cudaStream_t s) {
     if (a.y1 <= a.y0) return cudaSuccess;
+    if (a.K == kFK) {
+        TileGridArgs g{};
+        g.a = a;
+        bool paper = false;
+        if (a.n_dy == 7) {
+            int seen = 0;
+            for (int i = 0; i < 7; ++i) {
+                const int o = a.dys_host[i];
+                const int idx = o == -7 ? 0 : o == -3 ? 1 : o == -1 ? 2 : o == 0 ? 3 : o == 1 ? 4 : o == 3 ? 5 : o == 7 ? 6 : -1;
+                if (idx >= 0) seen |= 1 << idx;
+            }
+            paper = seen == 0x7f;
+        }
+        const int S = a.full_hi;
+        if (paper) {
+            g.n_dy = 7;
+            for (int i = 0; i < 7; ++i) g.dys[i] = a.dys_host[i];
+            g.n_groups = 1;
+            g.n_last = 7;
+            g.maxd = 7;
+            g.S = S;
+            g.n_total = 49;
+            return launch_tile_p<0>(g, s);
+        }
+        if (a.n_dy == 0) {
+            const int n = a.full_hi - a.full_lo + 1;
+            g.n_dy = n;
+            g.lo = a.full_lo;
+            g.n_groups = (n + 6) / 7;
+            g.n_last = n - 7 * (g.n_groups - 1);
+            g.maxd = S;
+            g.S = S;
+            g.n_total = n * n;
+            return launch_tile_p<1>(g, s);
+        }
+    }
     DeltaSet ds{};
     ds.n = a.n_dy;
     ds.lo = a.full_lo;

@@ -230,6 +230,221 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
     }
 }
 
+// ---------------------------------------------------------------------------
+// Quarter-sampling body (K = 8, forward ME, interior tiles): DESIGN.md "K1 me_quad".
+//
+// With a quarter mask every 2x2 block b holds exactly one measured pixel at
+// (dy_b, dx_b), so for a candidate v the only non-zero D_v
+// of block b is d_b = phi(c_b - ref(pos_b + v)).  Split d_b into four channels
+// G_c (c = 2 dy + dx, one non-zero).  For an output p = (2i+sy, 2j+sx) the 8x8
+// window covers block rows i-2..i+1 (sy = 0), or for sy = 1 the dy=1 pixels of
+// rows i-2..i+1 and the dy=0 pixels of rows i-1..i+2 (likewise columns), so
+//   E(2i,  2j  ) = V[C0](i) + V[C1](i)        C0 = G0+G1, C1 = G2+G3 (by dy)
+//   E(2i,  2j+1) = V[D0](i) + V[D1](i)        D0(k) = G1(k)+G0(k+1), D1(k) = G3(k)+G2(k+1)
+//   E(2i+1,2j  ) = V[C1](i) + V[C0](i+1)
+//   E(2i+1,2j+1) = V[D1](i) + V[D0](i+1)
+// where H[X](i,j) = sum_{k=j-2}^{j+1} X(i,k) and V[X](i) = sum_{h=i-2}^{i+1} H[X](h).
+// All box sums are 4-wide on the block grid (a quarter of the pixels), done as
+// pairwise trees (no subtraction: exact for uint8 data, order-fixed for float).
+// Producer warps 0-3 form d, the channel series and H (one warp per 9 block
+// columns, one lane per block row); consumer warps 4-7 form V, E and the
+// running argmin (one lane per block column, 7 block rows per warp), handing
+// H over through a 2-stage shared ring guarded by named barriers.
+// ---------------------------------------------------------------------------
+constexpr int kQBX = kTX / 2;           // 32 block columns per tile
+constexpr int kQBY = kTY / 2;           // 28 block rows per tile
+constexpr int kQHR = kQBY + 4;          // 32 H rows (block rows -2 .. 29)
+constexpr int kQHC = kQBX;              // 32 H columns (D already carries the k+1 block)
+constexpr int kQHP = kQHC + 1;          // H row pitch in float4 (odd: conflict-free STS.128 / LDS.128)
+constexpr int kQRun = 8;                // H columns per producer warp (4 x 8 = 32)
+constexpr int kQG = kQRun + 4;          // blocks read per producer lane (12: k = j-2 .. j+1, +1 for D)
+constexpr int kQSeg = kQBY / 4;         // 7 output block rows per consumer warp
+constexpr int kQWinRows = 2 * kQHR;     // 64 pixel rows of blocks per tile (+ alpha range)
+constexpr int kQWinCols = 2 * (4 * kQRun + 4);  // 72 pixel columns (blocks -2 .. 33)
+
+// Named barriers with immediate ids (1..4), so ptxas reserves only the ones used.
+template <int ID>
+__device__ __forceinline__ void nb_sync_i() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(kNT) : "memory"); }
+template <int ID>
+__device__ __forceinline__ void nb_arrive_i() { asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(kNT) : "memory"); }
+__device__ __forceinline__ void nb_sync(int id, int) {
+    switch (id) {
+        case 1: nb_sync_i<1>(); break;
+        case 2: nb_sync_i<2>(); break;
+        case 3: nb_sync_i<3>(); break;
+        default: nb_sync_i<4>(); break;
+    }
+}
+__device__ __forceinline__ void nb_arrive(int id, int) {
+    switch (id) {
+        case 1: nb_arrive_i<1>(); break;
+        case 2: nb_arrive_i<2>(); break;
+        case 3: nb_arrive_i<3>(); break;
+        default: nb_arrive_i<4>(); break;
+    }
+}
+
+// 1 iff every block the quad body reads (rows -2..29, cols -2..34) holds exactly one measured pixel.
+__device__ __forceinline__ bool quad_mask_ok(const BoxArgs &a, int px0, int py0) {
+    bool ok = true;
+    constexpr int NR = kQHR, NC = kQBX + 4;   // 32 x 36 blocks: rows -2..29, cols -2..33
+    for (int i = threadIdx.x; i < NR * NC; i += kNT) {
+        const int bi = i / NC - 2, bk = i % NC - 2;
+        const int y = py0 + 2 * bi, x = px0 + 2 * bk;
+        const int64_t r = (int64_t)(y - a.buf_y0) * a.mask.pitch;
+        const int n = a.mask.p[r + x] + a.mask.p[r + x + 1] + a.mask.p[r + a.mask.pitch + x] +
+                      a.mask.p[r + a.mask.pitch + x + 1];
+        ok = ok && (n == 1);
+    }
+    return __syncthreads_and(ok);
+}
+
+template <bool SSD>
+__device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0) {
+    const int alo = -a.S + chunk * kChunkRows;
+    const int ahi = min(a.S, alo + kChunkRows - 1);
+    const int nrow_b = kQWinRows + (ahi - alo);
+    const int ncol_b = kQWinCols + 2 * a.S;
+    const int bpitch = ncol_b | 1;
+    float *Bw = smem;
+    float4 *Hq = reinterpret_cast<float4 *>(smem + ((nrow_b * bpitch + 3) & ~3));   // [2][kQHR][kQHP]
+
+    // Stage the chunk's reference window: rows py0-4+alo .., cols px0-4-S ..
+    const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
+    for (int i = threadIdx.x; i < nrow_b * ncol_b; i += kNT) {
+        const int r = i / ncol_b, c = i - r * ncol_b;
+        Bw[r * bpitch + c] = load_ref(a, by0 + r, bx0 + c);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k0 = a.chunk_off[chunk], k1 = a.chunk_off[chunk + 1];
+
+    if (warp < 4) {
+        // ------------------------------ producer ------------------------------
+        const int hr = lane;               // H row = block row + 2
+        const int bi = hr - 2;
+        float cv[kQG], wy[kQG], wx[kQG], wxc[kQG];
+        int ad[kQG];   // byte offset of the block's measured pixel in the window (candidate (alo, 0))
+#pragma unroll
+        for (int kk = 0; kk < kQG; ++kk) {
+            const int bk = kQRun * warp - 2 + kk;
+            const int y = py0 + 2 * bi, x = px0 + 2 * bk;
+            const int64_t r = (int64_t)(y - a.buf_y0);
+            const uint8_t *m0 = a.mask.p + r * a.mask.pitch + x;
+            const int q = m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
+            const int dy = q >> 1, dx = q & 1;
+            cv[kk] = (float)a.cur.p[(r + dy) * a.cur.pitch + x + dx];
+            wy[kk] = (float)dy;
+            wx[kk] = (float)dx;
+            wxc[kk] = (float)(1 - dx);
+            ad[kk] = 4 * ((2 * bi + dy + 4) * bpitch + (2 * bk + dx + 4 + a.S));
+        }
+        for (int k = k0; k < k1; ++k) {
+            const int pk = __ldg(a.chunked + k);
+            const int al = (int)(int8_t)(pk & 0xff);
+            const int bt = (int)(int8_t)((pk >> 8) & 0xff);
+            const int s = (k - k0) & 1;
+            const char *bwc = reinterpret_cast<const char *>(Bw + (al - alo) * bpitch + bt);   // uniform
+            float t0[kQG], t1[kQG], m0s[kQG - 1], m1s[kQG - 1];
+            float g1p = 0.f, g3p = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < kQG; ++kk) {
+                const float dd = cv[kk] - *reinterpret_cast<const float *>(bwc + ad[kk]);
+                const float d = SSD ? __fmul_rn(dd, dd) : fabsf(dd);
+                const float u1 = __fmul_rn(d, wy[kk]);       // dy = 1 part (exactly d or 0)
+                const float u0 = __fsub_rn(d, u1);            // dy = 0 part
+                t0[kk] = u0;
+                t1[kk] = u1;
+                if (kk > 0) {
+                    // D0(k-1) = G1(k-1) + G0(k), G0(k) = u0(k) (1-dx(k)): the product is exact, so
+                    // the FMA rounds once, exactly like the add of the two channel values.
+                    m0s[kk - 1] = __fmaf_rn(u0, wxc[kk], g1p);
+                    m1s[kk - 1] = __fmaf_rn(u1, wxc[kk], g3p);
+                }
+                g1p = __fmul_rn(u0, wx[kk]);                  // G1(k) = dy0, dx1 channel
+                g3p = __fmul_rn(u1, wx[kk]);                  // G3(k) = dy1, dx1 channel
+            }
+            // 4-wide horizontal box (pairwise): H(m) = (X(m)+X(m+1)) + (X(m+2)+X(m+3)), m = 0..8
+            float4 hv[kQRun];
+            {
+                float p0[kQG - 1], p1[kQG - 1], p2[kQG - 2], p3[kQG - 2];
+#pragma unroll
+                for (int kk = 0; kk < kQG - 1; ++kk) {
+                    p0[kk] = __fadd_rn(t0[kk], t0[kk + 1]);
+                    p1[kk] = __fadd_rn(t1[kk], t1[kk + 1]);
+                }
+#pragma unroll
+                for (int kk = 0; kk < kQG - 2; ++kk) {
+                    p2[kk] = __fadd_rn(m0s[kk], m0s[kk + 1]);
+                    p3[kk] = __fadd_rn(m1s[kk], m1s[kk + 1]);
+                }
+#pragma unroll
+                for (int m = 0; m < kQRun; ++m)
+                    hv[m] = make_float4(__fadd_rn(p0[m], p0[m + 2]), __fadd_rn(p1[m], p1[m + 2]),
+                                        __fadd_rn(p2[m], p2[m + 2]), __fadd_rn(p3[m], p3[m + 2]));
+            }
+            if (k - k0 >= 2) nb_sync(3 + s, kNT);            // EMPTY[s]: consumers released stage s
+            float4 *hrow = Hq + (s * kQHR + hr) * kQHP + kQRun * warp;
+#pragma unroll
+            for (int m = 0; m < kQRun; ++m) hrow[m] = hv[m];
+            nb_arrive(1 + s, kNT);                           // FULL[s]
+        }
+        // drain: match the consumers' last EMPTY arrivals
+        for (int k = max(k0, k1 - 2); k < k1; ++k) nb_sync(3 + ((k - k0) & 1), kNT);
+    } else {
+        // ------------------------------ consumer ------------------------------
+        const int j = lane;                   // block column
+        const int seg = warp - 4;             // block rows 7*seg .. 7*seg+6
+        float be[kQSeg][4];
+        int br[kQSeg][4];
+#pragma unroll
+        for (int r = 0; r < kQSeg; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { be[r][c] = INFINITY; br[r][c] = -1; }
+        for (int k = k0; k < k1; ++k) {
+            const int rank = __ldg(a.chunked + k) >> 16;
+            const int s = (k - k0) & 1;
+            nb_sync(1 + s, kNT);                             // FULL[s]
+            const float4 *hcol = Hq + (s * kQHR + kQSeg * seg) * kQHP + j;
+            float4 h[kQSeg + 4];
+#pragma unroll
+            for (int t = 0; t < kQSeg + 4; ++t) h[t] = hcol[t * kQHP];
+            nb_arrive(3 + s, kNT);                           // EMPTY[s]
+            // V(i) = (H(i-2)+H(i-1)) + (H(i)+H(i+1)) for i = 0..7 (H index t = i+2 relative)
+            float4 p[kQSeg + 3];
+#pragma unroll
+            for (int t = 0; t < kQSeg + 3; ++t)
+                p[t] = make_float4(__fadd_rn(h[t].x, h[t + 1].x), __fadd_rn(h[t].y, h[t + 1].y),
+                                   __fadd_rn(h[t].z, h[t + 1].z), __fadd_rn(h[t].w, h[t + 1].w));
+            float4 v[kQSeg + 1];
+#pragma unroll
+            for (int i = 0; i < kQSeg + 1; ++i)
+                v[i] = make_float4(__fadd_rn(p[i].x, p[i + 2].x), __fadd_rn(p[i].y, p[i + 2].y),
+                                   __fadd_rn(p[i].z, p[i + 2].z), __fadd_rn(p[i].w, p[i + 2].w));
+#pragma unroll
+            for (int r = 0; r < kQSeg; ++r) {
+                const float e00 = __fadd_rn(v[r].x, v[r].y);
+                const float e01 = __fadd_rn(v[r].z, v[r].w);
+                const float e10 = __fadd_rn(v[r].y, v[r + 1].x);
+                const float e11 = __fadd_rn(v[r].w, v[r + 1].z);
+                if (e00 < be[r][0]) { be[r][0] = e00; br[r][0] = rank; }
+                if (e01 < be[r][1]) { be[r][1] = e01; br[r][1] = rank; }
+                if (e10 < be[r][2]) { be[r][2] = e10; br[r][2] = rank; }
+                if (e11 < be[r][3]) { be[r][3] = e11; br[r][3] = rank; }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kQSeg; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int py = py0 + 2 * (kQSeg * seg + r) + (c >> 1), px = px0 + 2 * j + (c & 1);
+                if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
+                const unsigned long long key = ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
+                atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+            }
+    }
+}
+
 template <int K, bool EXACT, bool SSD, bool REV>
 __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
     extern __shared__ __align__(16) float smem[];
@@ -244,6 +459,17 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
     if constexpr (REV) {
         box_body<K, EXACT, true, SSD, true>(a, smem, chunk, px0, py0);
     } else {
+        if constexpr (K == 8) {
+            // Quarter-sampling body: every pixel it touches, for every candidate, lies in the frame
+            // and in the caller's buffer window, and every block holds exactly one measurement.
+            const bool geom = a.S >= 4 && (py0 - 4 - a.S >= 0) && (py0 + 2 * kQHR - 5 + a.S <= a.H - 1) &&
+                              (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1) &&
+                              (py0 - 4 - a.S >= a.buf_y0) && (py0 + 2 * kQHR - 5 + a.S < a.buf_y0 + a.buf_rows);
+            if (geom && quad_mask_ok(a, px0, py0)) {
+                quad_body<SSD>(a, smem, chunk, px0, py0);
+                return;
+            }
+        }
         if (interior) box_body<K, EXACT, false, SSD, false>(a, smem, chunk, px0, py0);
         else box_body<K, EXACT, true, SSD, false>(a, smem, chunk, px0, py0);
     }
@@ -254,7 +480,12 @@ cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
     using G = BoxGeom<K>;
     const int nrow_b = G::HR + kChunkRows - 1;
     const int bpitch = (kTX + K - 1 + 2 * a.S) | 1;
-    const size_t smem = sizeof(float) * ((size_t)((nrow_b * bpitch + 3) & ~3) + 4 * (size_t)G::HR * kTXP);
+    size_t smem = sizeof(float) * ((size_t)((nrow_b * bpitch + 3) & ~3) + 4 * (size_t)G::HR * kTXP);
+    if (K == 8 && !REV) {
+        const int qrows = kQWinRows + kChunkRows - 1, qpitch = (kQWinCols + 2 * a.S) | 1;
+        const size_t qs = sizeof(float) * (size_t)((qrows * qpitch + 3) & ~3) + sizeof(float4) * 2 * kQHR * kQHP;
+        smem = smem > qs ? smem : qs;
+    }
     auto fn = box_kernel<K, EXACT, SSD, REV>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

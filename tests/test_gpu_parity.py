@@ -97,6 +97,42 @@ def test_fuzz_checks_u8_staged(seed):
     assert np.array_equal(st, oracle.nnc(o))
 
 
+def _perturbed_field(inp, K, S, seed, frac=0.15, ssd=False):
+    """Oracle ME field with a fraction of vectors replaced by random ones; (err, count) re-scored
+    with the forward cost so the field stays consistent (identity P4)."""
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=K, S=S, ssd=ssd)
+    rng = np.random.default_rng(seed)
+    ys, xs = np.nonzero(o["status"] == oracle.CANDIDATE)
+    pick = rng.random(ys.size) < frac
+    for y, x in zip(ys[pick], xs[pick]):
+        a, b = (int(v) for v in rng.integers(-S, S + 1, 2))
+        e, n = oracle.cost_fwd(inp["cur"], inp["cur_mask"], inp["ref"], y, x, a, b, K=K, ssd=ssd)
+        if n < 8:
+            continue
+        o["alpha"][y, x], o["beta"][y, x], o["err"][y, x], o["count"][y, x] = a, b, e, n
+    return o
+
+
+@pytest.mark.parametrize("seed,f32,ssd", [(0, False, False), (1, True, False), (2, False, True), (3, True, True)])
+def test_frmc_rmc_tiled_k8_perturbed(seed, f32, ssd):
+    """The tiled K=8 reverse-grid kernel (paper offsets / RMC groups) on fields with wrong vectors."""
+    inp = synth.rank_free_random_instance(900 + seed, 56, 44, ref_f32=f32, smooth=True)
+    S = 9
+    o = _perturbed_field(inp, 8, S, seed, ssd=ssd)
+    kw = dict(K=8, S=S, ssd=ssd)
+    st, ev = gpu_check("frmc", inp, o, **kw)
+    ost, oev = oracle.frmc(inp["cur"], inp["cur_mask"], inp["ref"], o, **kw)
+    assert np.array_equal(st, ost) and ev == oev
+    assert (ost == oracle.REJECTED).sum() > 0 and (ost == oracle.ACCEPTED).sum() > 0
+    st, ev = gpu_check("rmc", inp, o, **kw)
+    ost, oev = oracle.rmc(inp["cur"], inp["cur_mask"], inp["ref"], o, **kw)
+    assert np.array_equal(st, ost) and ev == oev
+    # Offsets given in another order: same decisions (a set, PAPER.md:104).
+    st2, _ = gpu_check("frmc", inp, o, offsets=(7, 3, 1, 0, -1, -3, -7), **kw)
+    ost2, _ = oracle.frmc(inp["cur"], inp["cur_mask"], inp["ref"], o, offsets=(7, 3, 1, 0, -1, -3, -7), **kw)
+    assert np.array_equal(st2, ost2)
+
+
 def test_nnc_golden_on_gpu(golden):
     g = golden("nnc_hand.json")
     for case in g["cases"]:
@@ -154,6 +190,31 @@ def test_f32_me_tolerance(S, K, ssd):
     o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=K, S=S, ssd=ssd)
     ties = f32_me_compare(g, o, inp, K, S, ssd=ssd)
     assert len(ties) <= max(3, int(1e-3 * (o["status"] == oracle.CANDIDATE).sum())), ties
+
+
+def test_f32_quad_tiles_tolerance():
+    """A frame large enough for interior quarter-sampling tiles (the K=8 block-grid body)."""
+    seq = synth.make_sequence(4, w=384, h=256)
+    inp = synth.pair_inputs(seq, 5, 1)
+    g, _ = gpu_me(inp, K=8, S=16)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=8, S=16)
+    ties = f32_me_compare(g, o, inp, 8, 16)
+    assert len(ties) <= max(3, int(1e-3 * (o["status"] == oracle.CANDIDATE).sum())), ties
+
+
+def test_non_quarter_mask_falls_back_bit_exact():
+    """Masks that are not quarter masks (two or zero measurements per 2x2 block) take the
+    generic body inside the same launch; results stay bit-exact."""
+    rng = np.random.default_rng(77)
+    W, H = 352, 288
+    inp = synth.rank_free_random_instance(77, W, H, smooth=True)
+    m = (rng.random((H, W)) < 0.3).astype(np.uint8)
+    m[100:160, 100:200] = synth.quarter_mask(100, 60, 5, False)   # mixed: quarter patch inside
+    inp["cur_mask"] = m
+    inp["cur"] = (inp["dense_cur"] * m).astype(np.uint8)
+    g, _ = gpu_me(inp, K=8, S=16)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=8, S=16)
+    assert_field_equal(g, o, what="non-quarter mask")
 
 
 def test_f32_checks_bit_exact_given_field():

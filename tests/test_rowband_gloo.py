@@ -1,0 +1,70 @@
+"""Row-band sharding on CPU: band geometry and the halo exchange over gloo."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2203_09200_b200 import rowband
+
+
+def test_band_geometry_covers_frame():
+    for H, G in ((1080, 1), (1080, 2), (1080, 4), (1080, 8), (2160, 8), (288, 3)):
+        h = rowband.halo_rows(24, 8)
+        if G > 1 and H // G < h:
+            continue
+        bands = [rowband.band_of(r, G, H, h) for r in range(G)]
+        assert bands[0].y0 == 0 and bands[-1].y1 == H
+        for a, b in zip(bands, bands[1:]):
+            assert a.y1 == b.y0 and a.y1 % 2 == 0          # contiguous, even (2x2 blocks stay whole)
+        for b in bands:
+            assert b.b0 == max(0, b.y0 - h) and b.b1 == min(H, b.y1 + h)
+    assert rowband.halo_rows(24, 8) == 30
+
+
+def test_thin_band_rejected():
+    with pytest.raises(ValueError):
+        rowband.band_of(1, 8, 64, rowband.halo_rows(24, 8))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, H, W, h, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        band = rowband.band_of(rank, world, H, h)
+        glob = torch.arange(H * W, dtype=torch.float32).reshape(H, W)
+        plane = torch.full((band.rows, W), float("nan"))
+        plane[band.y0 - band.b0:band.y1 - band.b0] = glob[band.y0:band.y1]   # only owned rows exist
+        rowband.exchange_halo(plane, band)
+        ok = torch.equal(plane, glob[band.b0:band.b1])
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_gloo(world):
+    H, W = 120, 16
+    h = rowband.halo_rows(8, 8)     # 14 rows
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, h, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res

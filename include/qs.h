@@ -26,7 +26,7 @@
  *   frame rows [buf_y0, buf_y0 + buf_rows); row r of a buffer is global row
  *   buf_y0 + r.  Work is produced for global rows [y_begin, y_end).  All border
  *   rules use the FULL frame (frame_w, frame_h) -- a band edge is not a border
- *   (reading R25).  roi == NULL means the whole frame, buf_y0 = 0.
+ *   (reading R25).  roi is required (it carries the frame size); QS_EINVAL if NULL.
  * - Pitches: image pitches are in BYTES and must be multiples of 16, base
  *   pointers 16-byte aligned (QS_EALIGN otherwise); the qs_field pitch is in
  *   ELEMENTS and shared by its five planes.
@@ -119,7 +119,7 @@ typedef struct {
  *                  neighbour (paper: "at most one" -> 1)
  *   frmc           run FRMC on the entries left checkable
  *   offsets        HOST array of per-axis FRMC offsets; must contain 0 and
- *                  satisfy |o| <= 32 (paper: {-7,-3,-1,0,1,3,7})
+ *                  satisfy |o| <= S (paper: {-7,-3,-1,0,1,3,7})
  *   n_offsets      1..15
  * With nnc and frmc both set this is the paper's cascade NNC -> FRMC: NNC
  * rejects, FRMC decides the NNC survivors (R16). */
@@ -248,7 +248,7 @@ int qs_project(const qs_field *f, const uint8_t *past_val, const uint8_t *past_m
  * While enabled, every kernel launched by the entry points above is bracketed
  * by two CUDA events recorded on its own stream.  qs_profile_read synchronises
  * the recorded events and returns the summed device time and the launch count
- * of one kernel ("me_box", "finalize", "nnc", "revgrid", "rme_decide",
+ * of one kernel ("me_box", "epilogue", "finalize", "nnc", "revgrid", "rme_decide",
  * "project") or of all of them ("*").  qs_profile_reset drops the records.
  * Process-global; calls from several threads are serialised internally.
  * ------------------------------------------------------------------------- */

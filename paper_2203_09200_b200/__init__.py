@@ -127,7 +127,7 @@ def qs_profile_reset():
     lib().qs_profile_reset()
 
 
-PROFILE_KERNELS = ("me_box", "finalize", "nnc", "revgrid", "rme_decide", "project")
+PROFILE_KERNELS = ("me_box", "finalize", "nnc", "revgrid", "rme_decide", "project", "epilogue")
 
 
 def _check(rc: int):

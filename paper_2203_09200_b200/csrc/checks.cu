@@ -7,6 +7,7 @@
 #include <cmath>
 
 #include "qs_internal.cuh"
+#include "tile_regions.cuh"
 
 namespace qs {
 namespace {
@@ -196,15 +197,8 @@ __global__ void revgrid_kernel(RevGridArgs a, DeltaSet ds) {
 // Delta_x patterns: PAT 0 = the paper's {-7,-3,-1,0,1,3,7},
 // PAT 1 = 7 consecutive values (RMC's [-S, S] in groups).
 // ---------------------------------------------------------------------------
-constexpr int kFT = 16;          // tile edge (entries)
-constexpr int kFK = 8;           // template
-constexpr int kFSeg = kFK + 14;  // current-row segment per item (22)
-
-template <int PAT>
-__device__ __forceinline__ constexpr int pat_j(int k) {
-    // column of delta_x within the 15-wide group span (delta_x - dx0)
-    return PAT == 0 ? (k == 0 ? 0 : k == 1 ? 4 : k == 2 ? 6 : k == 3 ? 7 : k == 4 ? 8 : k == 5 ? 10 : 14) : k;
-}
+using tile::kFT;
+using tile::kFK;
 
 struct TileGridArgs {
     RevGridArgs a;
@@ -222,53 +216,17 @@ template <int PAT, bool SSD, bool F32>
 __global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g) {
     extern __shared__ __align__(16) float sm[];
     const RevGridArgs &a = g.a;
-    constexpr int KL = kFK / 2;
     const int tx0 = blockIdx.x * kFT, ty0 = a.y0 + blockIdx.y * kFT;
-    // Regions (global coords of their row/col 0) and sizes.
-    const int cy0 = ty0 - g.maxd - KL, cx0 = tx0 - g.maxd - KL;
-    const int CR = kFT + 2 * g.maxd + kFK - 1, CC = CR;
-    const int ry0 = ty0 - g.S - KL, rx0 = tx0 - g.S - KL;
-    const int RR = kFT + 2 * g.S + kFK - 1, RC = RR;
-    const int cpitch = CC + 16 + 1;          // room for a 22-wide read past the region edge
-    const int rpitch = RC + 1;
-    const int mwords = (CC + 16 + 31) / 32 + 1;
-    float *Cs = sm;
-    float *Rs = Cs + CR * cpitch;
-    uint32_t *Mb = reinterpret_cast<uint32_t *>(Rs + RR * rpitch);
-    int *ent = reinterpret_cast<int *>(Mb + CR * mwords);   // packed entries [256]
+    const tile::Regions R = tile::layout(sm, ty0, tx0, g.maxd, g.S, a.W, a.H);
+    const tile::RegionSizes Z(g.maxd, g.S);
+    int *ent = reinterpret_cast<int *>(reinterpret_cast<char *>(sm) + Z.bytes());   // packed entries [256]
     float *ent_m0 = reinterpret_cast<float *>(ent + kFT * kFT);
     uint32_t *ent_e0 = reinterpret_cast<uint32_t *>(ent_m0 + kFT * kFT);
     uint8_t *rej = reinterpret_cast<uint8_t *>(ent_e0 + kFT * kFT);
     __shared__ int n_ent;
     const int tid = threadIdx.x;
     if (tid == 0) n_ent = 0;
-    for (int i = tid; i < CR * mwords; i += blockDim.x) Mb[i] = 0u;
-    __syncthreads();
-    // Stage the current region (NaN where unmeasured / outside) and its mask bits.
-    for (int i = tid; i < CR * cpitch; i += blockDim.x) {
-        const int r = i / cpitch, c = i - r * cpitch;
-        const int gy = cy0 + r, gx = cx0 + c;
-        float v = __int_as_float(0x7fc00000);
-        if (c < CC && gy >= 0 && gy < a.H && gx >= 0 && gx < a.W && gy >= a.buf_y0 && gy < a.buf_y0 + a.buf_rows) {
-            const int64_t rr = gy - a.buf_y0;
-            if (a.mask.p[rr * a.mask.pitch + gx]) {
-                v = (float)a.cur.p[rr * a.cur.pitch + gx];
-                atomicOr(&Mb[r * mwords + (c >> 5)], 1u << (c & 31));
-            }
-        }
-        Cs[i] = v;
-    }
-    // Stage the reference region (NaN outside the frame / buffer).
-    for (int i = tid; i < RR * rpitch; i += blockDim.x) {
-        const int r = i / rpitch, c = i - r * rpitch;
-        const int gy = ry0 + r, gx = rx0 + c;
-        float v = __int_as_float(0x7fc00000);
-        if (c < RC && gy >= 0 && gy < a.H && gx >= 0 && gx < a.W && gy >= a.buf_y0 && gy < a.buf_y0 + a.buf_rows) {
-            const int64_t rr = gy - a.buf_y0;
-            v = F32 ? reinterpret_cast<const float *>(a.ref.p + rr * a.ref.pitch)[gx] : (float)a.ref.p[rr * a.ref.pitch + gx];
-        }
-        Rs[i] = v;
-    }
+    tile::stage<F32>(R, a.cur, a.mask, a.ref, a.W, a.H, a.buf_y0, a.buf_rows);
     // Checkable entries of the tile.
     {
         const int ly = tid / kFT, lx = tid % kFT;
@@ -296,67 +254,21 @@ __global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g)
     const int per_entry = g.n_dy * g.n_groups;
     const int items = ne * per_entry;
     for (int it = tid; it < items; it += blockDim.x) {
-        const int e = it / per_entry;
+        // (delta_y, group)-major: later rounds skip entries an earlier round already rejected.
+        const int rem = it / ne, e = it - rem * ne;
         if (rej[e]) continue;                            // decision already made ("reject iff any")
-        const int rem = it - e * per_entry;
         const int iy = rem / g.n_groups, grp = rem - iy * g.n_groups;
         const int pk = ent[e];
         const int ly = pk & 0xff, lx = (pk >> 8) & 0xff;
         const int va = (int)(int8_t)((pk >> 16) & 0xff), vb = (int)(int8_t)((pk >> 24) & 0xff);
-        const int dy = PAT == 0 ? g.dys[iy] : g.lo + iy;
+        // PAT 1 visits delta_y = 0, -1, 1, -2, 2, ... (small offsets reject wrong vectors first)
+        const int dy = PAT == 0 ? g.dys[iy] : ((iy & 1) ? -((iy + 1) >> 1) : (iy >> 1));
         const int dx0 = PAT == 0 ? -7 : g.lo + 7 * grp;
         const int nk = PAT == 0 ? 7 : (grp == g.n_groups - 1 ? g.n_last : 7);
-        float acc[7];
-        int cnt[7];
-#pragma unroll
-        for (int k = 0; k < 7; ++k) { acc[k] = 0.f; cnt[k] = 0; }
-        // Region coordinates of row 0 / col 0 of the windows.
-        const int crow = (ty0 + ly + dy - KL) - cy0, ccol = (tx0 + lx + dx0 - KL) - cx0;
-        const int rrow = (ty0 + ly + va - KL) - ry0, rcol = (tx0 + lx + vb - KL) - rx0;
-#pragma unroll 1
-        for (int oy = 0; oy < kFK; ++oy) {
-            const float *cp = Cs + (crow + oy) * cpitch + ccol;
-            const float *rp = Rs + (rrow + oy) * rpitch + rcol;
-            float c[kFSeg], r[kFK];
-#pragma unroll
-            for (int j = 0; j < kFSeg; ++j) c[j] = cp[j];
-            uint32_t rb = 0;
-#pragma unroll
-            for (int j = 0; j < kFK; ++j) {
-                r[j] = rp[j];
-                rb |= (r[j] == r[j]) ? (1u << j) : 0u;
-            }
-            const uint32_t *mw = Mb + (crow + oy) * mwords;
-            const int bo = ccol;
-            const uint32_t bits = __funnelshift_r(mw[bo >> 5], mw[(bo >> 5) + 1], bo & 31);
-#pragma unroll
-            for (int k = 0; k < 7; ++k) {
-                const int j = pat_j<PAT>(k);
-#pragma unroll
-                for (int ox = 0; ox < kFK; ++ox) {
-                    const float d = r[ox] - c[ox + j];
-                    const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
-                    acc[k] = __fadd_rn(acc[k], fmaxf(t, 0.f));     // NaN (no term) -> +0: exact no-op
-                }
-                cnt[k] += __popc((bits >> j) & rb);
-            }
-        }
-        bool reject = false;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) {
-            if (k >= nk) continue;
-            const int dx = dx0 + pat_j<PAT>(k);
-            if (dy == 0 && dx == 0) continue;
-            if (cnt[k] < a.min_support) continue;             // SENTINEL never rejects (R11)
-            if (F32) {
-                if (__fdiv_rn(acc[k], (float)cnt[k]) < ent_m0[e]) reject = true;
-            } else {
-                const unsigned long long ek = (unsigned long long)acc[k];
-                const unsigned n0 = (unsigned)__float_as_int(ent_m0[e]);
-                if (ek * n0 < (unsigned long long)ent_e0[e] * (unsigned)cnt[k]) reject = true;
-            }
-        }
-        if (reject) rej[e] = 1;
+        const uint32_t n0 = F32 ? ent_e0[e] : (uint32_t)__float_as_int(ent_m0[e]);
+        if (tile::frmc_item<PAT, SSD, F32>(R, ty0, tx0, ly, lx, va, vb, dy, dx0, nk, a.min_support, ent_m0[e],
+                                           ent_e0[e], n0))
+            rej[e] = 1;
     }
     __syncthreads();
     for (int e = tid; e < ne; e += blockDim.x) {
@@ -369,10 +281,7 @@ __global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g)
 
 template <int PAT, bool SSD, bool F32>
 cudaError_t launch_tile_t(const TileGridArgs &g, cudaStream_t s) {
-    const int CR = kFT + 2 * g.maxd + kFK - 1, CC = CR;
-    const int RR = kFT + 2 * g.S + kFK - 1, RC = RR;
-    const int cpitch = CC + 16 + 1, rpitch = RC + 1, mwords = (CC + 16 + 31) / 32 + 1;
-    const size_t smem = sizeof(float) * ((size_t)CR * cpitch + (size_t)RR * rpitch) + sizeof(uint32_t) * CR * mwords +
+    const size_t smem = tile::RegionSizes(g.maxd, g.S).bytes() +
                         (sizeof(int) + sizeof(float) + sizeof(uint32_t) + 1) * kFT * kFT + 16;
     auto fn = revgrid_tile_kernel<PAT, SSD, F32>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -467,7 +376,8 @@ cudaError_t launch_revgrid(const RevGridArgs &a, cudaStream_t s) {
         const int S = a.full_hi;
         if (paper) {
             g.n_dy = 7;
-            for (int i = 0; i < 7; ++i) g.dys[i] = a.dys_host[i];
+            const int8_t order[7] = {0, -1, 1, -3, 3, -7, 7};   // the same set; small offsets first
+            for (int i = 0; i < 7; ++i) g.dys[i] = order[i];
             g.n_groups = 1;
             g.n_last = 7;
             g.maxd = 7;

@@ -1,0 +1,247 @@
+// epilogue.cu -- the fused per-pair epilogue of qs_me_search for K = 8:
+//   finalize (decode the merged ME keys, re-sum the chosen vector's error in the
+//   definition's row-major order), NNC (Eq. 1; R14, R15) and the
+//   FRMC cascade (R11, R12, R16) in ONE launch per
+//   16x16 tile.  The tile's current-frame and reference regions are staged once in
+//   shared memory and serve all three steps; the motion vectors of the tile and its
+//   2-pixel halo are decoded from the ME keys directly (no round trip through the
+//   field planes), so the field is written once, with its final statuses.
+#include <cmath>
+
+#include "qs_internal.cuh"
+#include "tile_regions.cuh"
+
+namespace qs {
+namespace {
+
+using tile::kFK;
+using tile::kFT;
+constexpr int kH2 = kFT + 4;   // decoded window: tile + 2-pixel halo (NNC's vector halo)
+constexpr int kH1 = kFT + 2;   // filtered window: tile + 1-pixel halo
+
+__device__ __forceinline__ int lower_median9(int (&v)[9], int n) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8 - i; ++j) {
+            const int a = v[j], b = v[j + 1];
+            v[j] = min(a, b);
+            v[j + 1] = max(a, b);
+        }
+    int r = v[0];
+#pragma unroll
+    for (int i = 1; i < 9; ++i)
+        if (i == (n - 1) / 2) r = v[i];
+    return r;
+}
+
+struct EpiShared {
+    int8_t sa[kH2][kH2], sb[kH2][kH2];
+    uint8_t sv[kH2][kH2];
+    int fa[kH1][kH1], fb[kH1][kH1];
+    uint8_t st[kFT * kFT];
+    float m0[kFT * kFT];
+    uint32_t e0[kFT * kFT], n0[kFT * kFT];
+    int ent[kFT * kFT];
+    uint8_t rej[kFT * kFT];
+    int n_ent;
+};
+
+template <bool SSD, bool F32, bool NNC, bool FRMC>
+__global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
+    extern __shared__ __align__(16) float sm[];
+    __shared__ EpiShared S;
+    constexpr int KL = kFK / 2;
+    const int tx0 = blockIdx.x * kFT, ty0 = g.lo + blockIdx.y * kFT;
+    const tile::Regions R = tile::layout(sm, ty0, tx0, 7, g.S, g.W, g.H);
+    const int tid = threadIdx.x;
+    if (tid == 0) S.n_ent = 0;
+    tile::stage<F32>(R, g.cur, g.mask, g.ref, g.W, g.H, g.buf_y0, g.buf_rows);
+
+    // 1. Decode the vectors of the tile + 2-pixel halo from the keys; validity needs the
+    //    support n of the chosen vector (min_support, R6), counted from the mask bits.
+    for (int i = tid; i < kH2 * kH2; i += blockDim.x) {
+        const int r = i / kH2, c = i % kH2;
+        const int gy = ty0 - 2 + r, gx = tx0 - 2 + c;
+        int8_t va = 0, vb = 0;
+        uint8_t valid = 0, st0 = kNotTarget, nn = 0;
+        if (gy >= g.lo && gy < g.hi && gx >= 0 && gx < g.W) {
+            const int cr = gy - R.cy0, cc = gx - R.cx0;
+            const bool measured = (tile::mask_bits(R, cr, cc) & 1u) != 0;
+            if (!measured) {
+                st0 = kInvalid;
+                const unsigned long long key = g.keys[(int64_t)(gy - g.lo) * g.key_pitch + gx];
+                if (key != ~0ull) {
+                    const int pk = __ldg(g.canon + (int)(key & 0xffffffffu));
+                    const int a = (int)(int8_t)(pk & 0xff), b = (int)(int8_t)((pk >> 8) & 0xff);
+                    uint32_t colm = 0;
+#pragma unroll
+                    for (int j = 0; j < kFK; ++j) {
+                        const int qx = gx - KL + j;
+                        colm |= (qx >= 0 && qx < g.W && qx + b >= 0 && qx + b < g.W) ? (1u << j) : 0u;
+                    }
+                    int n = 0;
+#pragma unroll
+                    for (int oy = 0; oy < kFK; ++oy) {
+                        const int qy = gy - KL + oy;
+                        if (qy < 0 || qy >= g.H || qy + a < 0 || qy + a >= g.H) continue;
+                        n += __popc(tile::mask_bits(R, qy - R.cy0, gx - KL - R.cx0) & colm);
+                    }
+                    nn = (uint8_t)n;
+                    if (n >= g.min_support) {
+                        valid = 1;
+                        st0 = kCandidate;
+                        va = (int8_t)a;
+                        vb = (int8_t)b;
+                    }
+                }
+            }
+        }
+        S.sa[r][c] = va;
+        S.sb[r][c] = vb;
+        S.sv[r][c] = valid;
+        if (r >= 2 && r < kFT + 2 && c >= 2 && c < kFT + 2) {
+            const int o = (r - 2) * kFT + (c - 2);
+            S.st[o] = st0;
+            S.n0[o] = nn;
+        }
+    }
+    __syncthreads();
+
+    // 2. Filtered field (Eq. 1) on the tile + 1-pixel halo.
+    if (NNC) {
+        for (int i = tid; i < kH1 * kH1; i += blockDim.x) {
+            const int r = i / kH1 + 1, c = i % kH1 + 1;
+            int la[9], lb[9], n = 0;
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int k = (dy + 1) * 3 + (dx + 1);
+                    const bool ok = S.sv[r + dy][c + dx];
+                    la[k] = ok ? S.sa[r + dy][c + dx] : 1000;
+                    lb[k] = ok ? S.sb[r + dy][c + dx] : 1000;
+                    n += ok;
+                }
+            int ma = 0, mb = 0;
+            if (S.sv[r][c]) {
+                ma = lower_median9(la, n);
+                mb = lower_median9(lb, n);
+            }
+            S.fa[r - 1][c - 1] = ma;
+            S.fb[r - 1][c - 1] = mb;
+        }
+        __syncthreads();
+    }
+
+    // 3. Own entry: the chosen vector's error re-summed in row-major order (R23), NNC decision.
+    const int ly = tid / kFT, lx = tid % kFT;
+    const int gy = ty0 + ly, gx = tx0 + lx;
+    const bool own = gy < g.hi && gx < g.W;
+    const bool checked_row = gy >= g.y0 && gy < g.y1;
+    uint8_t st = S.st[tid];
+    const int a = S.sa[ly + 2][lx + 2], b = S.sb[ly + 2][lx + 2];
+    float ef = 0.f;
+    uint32_t eu = 0;
+    if (own && st == kCandidate) {
+        const int crow = (gy - KL) - R.cy0, ccol = (gx - KL) - R.cx0;
+        const int rrow = (gy + a - KL) - R.ry0, rcol = (gx + b - KL) - R.rx0;
+#pragma unroll 1
+        for (int oy = 0; oy < kFK; ++oy) {
+            const float *cp = R.Cs + (crow + oy) * R.cpitch + ccol;
+            const float *rp = R.Rs + (rrow + oy) * R.rpitch + rcol;
+#pragma unroll
+            for (int ox = 0; ox < kFK; ++ox) {
+                const float d = __fsub_rn(cp[ox], rp[ox]);
+                const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
+                ef = __fadd_rn(ef, fmaxf(t, 0.f));   // NaN (no term) -> +0
+            }
+        }
+        if (!F32) eu = (uint32_t)ef;                 // integer-valued and < 2^24: exact
+        if (NNC && checked_row) {
+            const int r = ly + 2, c = lx + 2;
+            const int ca = S.fa[r - 1][c - 1], cb = S.fb[r - 1][c - 1];
+            bool reject = false;
+            const int NB[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int rr = r + NB[k][0], cc = c + NB[k][1];
+                if (!S.sv[rr][cc]) continue;
+                if (abs(ca - S.fa[rr - 1][cc - 1]) + abs(cb - S.fb[rr - 1][cc - 1]) > g.nnc_threshold) reject = true;
+            }
+            st = reject ? kRejected : kAccepted;
+        }
+    }
+    if (FRMC) {
+        S.m0[tid] = F32 ? __fdiv_rn(ef, (float)S.n0[tid]) : 0.f;
+        S.e0[tid] = F32 ? 0u : eu;
+        S.rej[tid] = 0;
+        if (own && checked_row && (st == kCandidate || st == kAccepted)) {
+            const int slot = atomicAdd(&S.n_ent, 1);
+            S.ent[slot] = tid;
+        }
+    }
+    if (own) {
+        const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f.pitch + gx;
+        const bool has = st >= kCandidate;
+        g.f.alpha[fi] = has ? (int8_t)a : (int8_t)0;
+        g.f.beta[fi] = has ? (int8_t)b : (int8_t)0;
+        g.f.count[fi] = has ? S.n0[tid] : (uint8_t)0;
+        if (F32) reinterpret_cast<float *>(g.f.err)[fi] = has ? ef : 0.f;
+        else reinterpret_cast<uint32_t *>(g.f.err)[fi] = has ? eu : 0u;
+        if (!FRMC) g.f.status[fi] = st;
+    }
+    if (!FRMC) return;
+
+    // 4. FRMC on the checkable entries (NNC survivors in the cascade): items (entry, delta_y).
+    __syncthreads();
+    const int ne = S.n_ent;
+    const int items = ne * 7;
+    // delta_y-major: later rounds skip entries an earlier delta_y row already rejected.
+    for (int it = tid; it < items; it += blockDim.x) {
+        const int iy = it / ne, e = it - iy * ne;
+        const int o = S.ent[e];
+        if (S.rej[o]) continue;
+        const int ely = o / kFT, elx = o % kFT;
+        const int va = S.sa[ely + 2][elx + 2], vb = S.sb[ely + 2][elx + 2];
+        if (tile::frmc_item<0, SSD, F32>(R, ty0, tx0, ely, elx, va, vb, g.dys[iy], -7, 7, g.min_support, S.m0[o],
+                                         S.e0[o], S.n0[o]))
+            S.rej[o] = 1;
+    }
+    __syncthreads();
+    if (own) {
+        const bool checked = checked_row && (st == kCandidate || st == kAccepted);
+        const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f.pitch + gx;
+        g.f.status[fi] = checked ? (S.rej[tid] ? kRejected : kAccepted) : st;
+    }
+    if (g.evals && tid == 0 && ne) atomicAdd(g.evals, 49ull * (unsigned long long)ne);
+}
+
+template <bool SSD, bool F32, bool NNC, bool FRMC>
+cudaError_t launch_epi_t(const EpiArgs &g, cudaStream_t s) {
+    const size_t smem = tile::RegionSizes(7, g.S).bytes() + 16;
+    auto fn = epilogue_kernel<SSD, F32, NNC, FRMC>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grd((g.W + kFT - 1) / kFT, (g.hi - g.lo + kFT - 1) / kFT);
+    fn<<<grd, 256, smem, s>>>(g);
+    return cudaGetLastError();
+}
+
+template <bool SSD, bool F32>
+cudaError_t launch_epi_c(const EpiArgs &g, cudaStream_t s) {
+    if (g.nnc && g.frmc) return launch_epi_t<SSD, F32, true, true>(g, s);
+    if (g.nnc) return launch_epi_t<SSD, F32, true, false>(g, s);
+    if (g.frmc) return launch_epi_t<SSD, F32, false, true>(g, s);
+    return launch_epi_t<SSD, F32, false, false>(g, s);
+}
+
+}  // namespace
+
+cudaError_t launch_epilogue(const EpiArgs &g, cudaStream_t s) {
+    if (g.hi <= g.lo) return cudaSuccess;
+    if (g.ref_f32) return g.ssd ? launch_epi_c<true, true>(g, s) : launch_epi_c<false, true>(g, s);
+    return g.ssd ? launch_epi_c<true, false>(g, s) : launch_epi_c<false, false>(g, s);
+}
+
+}  // namespace qs

@@ -108,6 +108,7 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
     float *Bw = smem;
     float *Hs = smem + ((nrow_b * bpitch + 3) & ~3);
     float *Ns = Hs + 2 * G::HR * kTXP;
+    int *clist = reinterpret_cast<int *>(Ns + 2 * G::HR * kTXP);   // the chunk's candidates
 
     // Stage the chunk's B window: rows py0-KL+alo .., cols px0-KL-S ..
     const int by0 = py0 - G::KL + alo, bx0 = px0 - G::KL - a.S;
@@ -115,6 +116,8 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
         const int r = i / ncol_b, c = i - r * ncol_b;
         Bw[r * bpitch + c] = REV ? load_cur_masked(a, by0 + r, bx0 + c) : load_ref(a, by0 + r, bx0 + c);
     }
+    const int kg0 = a.chunk_off[chunk], nkc = a.chunk_off[chunk + 1] - kg0;
+    for (int i = threadIdx.x; i < nkc; i += kNT) clist[i] = __ldg(a.chunked + kg0 + i);
 
     // Phase-A role: H row ya, columns xa0 .. xa0+kRun-1; A values in registers.
     const int ta = threadIdx.x;
@@ -138,9 +141,9 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
     const float ms = (float)a.min_support;
 
     __syncthreads();
-    const int k0 = a.chunk_off[chunk], k1 = a.chunk_off[chunk + 1];
+    const int k0 = 0, k1 = nkc;
     for (int k = k0; k < k1; ++k) {
-        const int pk = __ldg(a.chunked + k);
+        const int pk = clist[k];
         const int al = (int)(int8_t)(pk & 0xff);
         const int bt = (int)(int8_t)((pk >> 8) & 0xff);
         const int rank = pk >> 16;
@@ -272,7 +275,11 @@ __device__ __forceinline__ void nb_sync(int id, int) {
         case 1: nb_sync_i<1>(); break;
         case 2: nb_sync_i<2>(); break;
         case 3: nb_sync_i<3>(); break;
-        default: nb_sync_i<4>(); break;
+        case 4: nb_sync_i<4>(); break;
+        case 5: nb_sync_i<5>(); break;
+        case 6: nb_sync_i<6>(); break;
+        case 7: nb_sync_i<7>(); break;
+        default: nb_sync_i<8>(); break;
     }
 }
 __device__ __forceinline__ void nb_arrive(int id, int) {
@@ -280,9 +287,14 @@ __device__ __forceinline__ void nb_arrive(int id, int) {
         case 1: nb_arrive_i<1>(); break;
         case 2: nb_arrive_i<2>(); break;
         case 3: nb_arrive_i<3>(); break;
-        default: nb_arrive_i<4>(); break;
+        case 4: nb_arrive_i<4>(); break;
+        case 5: nb_arrive_i<5>(); break;
+        case 6: nb_arrive_i<6>(); break;
+        case 7: nb_arrive_i<7>(); break;
+        default: nb_arrive_i<8>(); break;
     }
 }
+constexpr int kQStages = 4;   // H ring depth: FULL[s] = barrier 1+s, EMPTY[s] = barrier 5+s
 
 // 1 iff every block the quad body reads (rows -2..29, cols -2..34) holds exactly one measured pixel.
 __device__ __forceinline__ bool quad_mask_ok(const BoxArgs &a, int px0, int py0) {
@@ -307,17 +319,20 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     const int ncol_b = kQWinCols + 2 * a.S;
     const int bpitch = ncol_b | 1;
     float *Bw = smem;
-    float4 *Hq = reinterpret_cast<float4 *>(smem + ((nrow_b * bpitch + 3) & ~3));   // [2][kQHR][kQHP]
+    float4 *Hq = reinterpret_cast<float4 *>(smem + ((nrow_b * bpitch + 3) & ~3));   // [kQStages][kQHR][kQHP]
+    int *clist = reinterpret_cast<int *>(Hq + kQStages * kQHR * kQHP);             // the chunk's candidates
 
-    // Stage the chunk's reference window: rows py0-4+alo .., cols px0-4-S ..
+    // Stage the chunk's reference window (rows py0-4+alo .., cols px0-4-S ..) and candidate list.
     const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
     for (int i = threadIdx.x; i < nrow_b * ncol_b; i += kNT) {
         const int r = i / ncol_b, c = i - r * ncol_b;
         Bw[r * bpitch + c] = load_ref(a, by0 + r, bx0 + c);
     }
+    const int k0g = a.chunk_off[chunk], nk = a.chunk_off[chunk + 1] - k0g;
+    for (int i = threadIdx.x; i < nk; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k0 = a.chunk_off[chunk], k1 = a.chunk_off[chunk + 1];
+    const int k0 = 0, k1 = nk;
 
     if (warp < 4) {
         // ------------------------------ producer ------------------------------
@@ -340,10 +355,10 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             ad[kk] = 4 * ((2 * bi + dy + 4) * bpitch + (2 * bk + dx + 4 + a.S));
         }
         for (int k = k0; k < k1; ++k) {
-            const int pk = __ldg(a.chunked + k);
+            const int pk = clist[k];
             const int al = (int)(int8_t)(pk & 0xff);
             const int bt = (int)(int8_t)((pk >> 8) & 0xff);
-            const int s = (k - k0) & 1;
+            const int s = (k - k0) & (kQStages - 1);
             const char *bwc = reinterpret_cast<const char *>(Bw + (al - alo) * bpitch + bt);   // uniform
             float t0[kQG], t1[kQG], m0s[kQG - 1], m1s[kQG - 1];
             float g1p = 0.f, g3p = 0.f;
@@ -383,14 +398,14 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                     hv[m] = make_float4(__fadd_rn(p0[m], p0[m + 2]), __fadd_rn(p1[m], p1[m + 2]),
                                         __fadd_rn(p2[m], p2[m + 2]), __fadd_rn(p3[m], p3[m + 2]));
             }
-            if (k - k0 >= 2) nb_sync(3 + s, kNT);            // EMPTY[s]: consumers released stage s
+            if (k - k0 >= kQStages) nb_sync(5 + s, kNT);     // EMPTY[s]: consumers released stage s
             float4 *hrow = Hq + (s * kQHR + hr) * kQHP + kQRun * warp;
 #pragma unroll
             for (int m = 0; m < kQRun; ++m) hrow[m] = hv[m];
             nb_arrive(1 + s, kNT);                           // FULL[s]
         }
         // drain: match the consumers' last EMPTY arrivals
-        for (int k = max(k0, k1 - 2); k < k1; ++k) nb_sync(3 + ((k - k0) & 1), kNT);
+        for (int k = max(k0, k1 - kQStages); k < k1; ++k) nb_sync(5 + ((k - k0) & (kQStages - 1)), kNT);
     } else {
         // ------------------------------ consumer ------------------------------
         const int j = lane;                   // block column
@@ -402,14 +417,14 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
 #pragma unroll
             for (int c = 0; c < 4; ++c) { be[r][c] = INFINITY; br[r][c] = -1; }
         for (int k = k0; k < k1; ++k) {
-            const int rank = __ldg(a.chunked + k) >> 16;
-            const int s = (k - k0) & 1;
+            const int rank = clist[k] >> 16;
+            const int s = (k - k0) & (kQStages - 1);
             nb_sync(1 + s, kNT);                             // FULL[s]
             const float4 *hcol = Hq + (s * kQHR + kQSeg * seg) * kQHP + j;
             float4 h[kQSeg + 4];
 #pragma unroll
             for (int t = 0; t < kQSeg + 4; ++t) h[t] = hcol[t * kQHP];
-            nb_arrive(3 + s, kNT);                           // EMPTY[s]
+            nb_arrive(5 + s, kNT);                           // EMPTY[s]
             // V(i) = (H(i-2)+H(i-1)) + (H(i)+H(i+1)) for i = 0..7 (H index t = i+2 relative)
             float4 p[kQSeg + 3];
 #pragma unroll
@@ -480,10 +495,12 @@ cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
     using G = BoxGeom<K>;
     const int nrow_b = G::HR + kChunkRows - 1;
     const int bpitch = (kTX + K - 1 + 2 * a.S) | 1;
-    size_t smem = sizeof(float) * ((size_t)((nrow_b * bpitch + 3) & ~3) + 4 * (size_t)G::HR * kTXP);
+    size_t smem = sizeof(float) * ((size_t)((nrow_b * bpitch + 3) & ~3) + 4 * (size_t)G::HR * kTXP) +
+                  sizeof(int) * kChunkRows * (2 * a.S + 1);
     if (K == 8 && !REV) {
         const int qrows = kQWinRows + kChunkRows - 1, qpitch = (kQWinCols + 2 * a.S) | 1;
-        const size_t qs = sizeof(float) * (size_t)((qrows * qpitch + 3) & ~3) + sizeof(float4) * 2 * kQHR * kQHP;
+        const size_t qs = sizeof(float) * (size_t)((qrows * qpitch + 3) & ~3) +
+                          sizeof(float4) * kQStages * kQHR * kQHP + sizeof(int) * kChunkRows * (2 * a.S + 1);
         smem = smem > qs ? smem : qs;
     }
     auto fn = box_kernel<K, EXACT, SSD, REV>;

@@ -43,8 +43,21 @@ std::map<std::pair<int, int>, qs::CandTables *> g_tabs;
 // ---------------------------------------------------------------------------
 // Profiler: CUDA events around each launch, on the launch stream.
 // ---------------------------------------------------------------------------
-enum ProfKernel { P_ME_BOX = 0, P_FINALIZE, P_NNC, P_REVGRID, P_RME_DECIDE, P_PROJECT, P_COUNT };
-const char *kProfNames[P_COUNT] = {"me_box", "finalize", "nnc", "revgrid", "rme_decide", "project"};
+enum ProfKernel { P_ME_BOX = 0, P_FINALIZE, P_NNC, P_REVGRID, P_RME_DECIDE, P_PROJECT, P_EPILOGUE, P_COUNT };
+const char *kProfNames[P_COUNT] = {"me_box", "finalize", "nnc", "revgrid", "rme_decide", "project", "epilogue"};
+
+// {-7,-3,-1,0,1,3,7}, in any order.
+bool is_paper_offsets(const int8_t *o, int n) {
+    if (n != 7) return false;
+    int seen = 0;
+    for (int i = 0; i < 7; ++i) {
+        const int v = o[i];
+        const int idx = v == -7 ? 0 : v == -3 ? 1 : v == -1 ? 2 : v == 0 ? 3 : v == 1 ? 4 : v == 3 ? 5 : v == 7 ? 6 : -1;
+        if (idx < 0) return false;
+        seen |= 1 << idx;
+    }
+    return seen == 0x7f;
+}
 
 struct ProfRec {
     int kernel;
@@ -335,6 +348,46 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
         e = launch_box(a, K, p->err == QS_SSD, false, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "me_box launch");
+
+    if (K == 8) {
+        // Fused epilogue: finalize + NNC + FRMC (the paper's offsets, in any order) in one launch.
+        const bool paper = frmc && is_paper_offsets(fuse->offsets, fuse->n_offsets);
+        EpiArgs g{};
+        g.cur = a.cur;
+        g.mask = a.mask;
+        g.ref = a.ref;
+        g.ref_f32 = a.ref_f32;
+        g.ssd = p->err == QS_SSD;
+        g.W = r.W;
+        g.H = r.H;
+        g.buf_y0 = r.b0;
+        g.buf_rows = r.br;
+        g.S = p->S;
+        g.min_support = p->min_support;
+        g.lo = lo;
+        g.hi = hi;
+        g.y0 = r.y0;
+        g.y1 = r.y1;
+        g.keys = keys;
+        g.key_pitch = r.W;
+        g.canon = t->canon;
+        g.f = view(out);
+        g.nnc = nnc;
+        g.nnc_threshold = nnc ? fuse->nnc_threshold : 0;
+        g.frmc = paper;
+        const int8_t order[7] = {0, -1, 1, -3, 3, -7, 7};   // the paper's set; small offsets first
+        for (int i = 0; paper && i < 7; ++i) g.dys[i] = order[i];
+        g.evals = eval_count;
+        {
+            ProfScope ps(P_EPILOGUE, s);
+            e = launch_epilogue(g, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "epilogue launch");
+        if (frmc && !paper)
+            return run_frmc(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, fuse->offsets, fuse->n_offsets, 0, out,
+                            eval_count, s);
+        return QS_OK;
+    }
 
     FinalizeArgs fa{};
     fa.cur = a.cur;

@@ -90,6 +90,23 @@ struct FieldView {
 cudaError_t launch_nnc(FieldView f, int W, int H, int buf_y0, int buf_rows, int y0, int y1, int threshold,
                        cudaStream_t s);
 
+// Fused per-pair epilogue for K = 8 (epilogue.cu): finalize + NNC + FRMC (paper offsets).
+struct EpiArgs {
+    Plane cur, mask, ref;
+    int ref_f32, ssd;
+    int W, H, buf_y0, buf_rows, S, min_support;
+    int lo, hi;                      // rows holding ME keys (finalized)
+    int y0, y1;                      // rows whose entries are checked
+    const unsigned long long *keys;  // keys row 0 == global row lo
+    int64_t key_pitch;
+    const int32_t *canon;
+    FieldView f;
+    int nnc, nnc_threshold, frmc;
+    int8_t dys[8];                   // FRMC delta_y order (a permutation of the paper's offsets)
+    unsigned long long *evals;
+};
+cudaError_t launch_epilogue(const EpiArgs &g, cudaStream_t s);
+
 struct RevGridArgs {
     Plane cur, mask, ref;
     int ref_f32, ssd, K;

@@ -1,0 +1,176 @@
+// tile_regions.cuh -- shared-memory staging of a 16x16 entry tile's current-frame and
+// reference regions, and the K = 8 reverse-cost worker used by FRMC / RMC
+// (checks.cu: revgrid_tile_kernel) and by the fused pair epilogue (epilogue.cu).
+//
+// Reverse cost (R9, R23): for an entry p with vector v and
+// delta, rc(p+v, -v+delta) = sum over o (row-major) of phi(ref(p+v+o) - cur(p+o+delta))
+// where p+v+o and p+o+delta are in the frame and cur_mask(p+o+delta) = 1.  Both regions
+// are staged as float with NaN marking "no term", so every excluded slot adds exactly +0
+// and each cost is the oracle's row-major fp32 sum.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "qs_internal.cuh"
+
+namespace qs {
+namespace tile {
+
+constexpr int kFT = 16;          // tile edge (entries)
+constexpr int kFK = 8;           // template
+constexpr int kFSeg = kFK + 14;  // current-row segment per FRMC item (22)
+
+// Column of delta_x within a 15-wide group span (delta_x - dx0).
+// PAT 0 = the paper's {-7,-3,-1,0,1,3,7}; PAT 1 = 7 consecutive values.
+template <int PAT>
+__device__ __forceinline__ constexpr int pat_j(int k) {
+    return PAT == 0 ? (k == 0 ? 0 : k == 1 ? 4 : k == 2 ? 6 : k == 3 ? 7 : k == 4 ? 8 : k == 5 ? 10 : 14) : k;
+}
+
+struct Regions {
+    int cy0, cx0, CR, CC, cpitch, mwords;   // current region: global row/col of element 0, sizes
+    int ry0, rx0, RR, RC, rpitch;           // reference region
+    float *Cs, *Rs;
+    uint32_t *Mb;                           // mask bits of the current region rows
+    int W, H;                               // frame
+};
+
+struct RegionSizes {
+    int CR, CC, cpitch, mwords, RR, RC, rpitch;
+    __host__ __device__ RegionSizes(int maxd, int S) {
+        constexpr int KL = kFK / 2;
+        (void)KL;
+        CR = kFT + 2 * maxd + kFK - 1;
+        CC = CR;
+        cpitch = CC + 16 + 1;   // room for a 22-wide read past the region edge
+        mwords = (CC + 16 + 31) / 32 + 1;
+        RR = kFT + 2 * S + kFK - 1;
+        RC = RR;
+        rpitch = RC + 1;
+    }
+    __host__ __device__ size_t bytes() const {
+        return sizeof(float) * ((size_t)CR * cpitch + (size_t)RR * rpitch) + sizeof(uint32_t) * (size_t)CR * mwords;
+    }
+};
+
+__device__ __forceinline__ Regions layout(float *sm, int ty0, int tx0, int maxd, int S, int W, int H) {
+    constexpr int KL = kFK / 2;
+    RegionSizes z(maxd, S);
+    Regions g;
+    g.W = W;
+    g.H = H;
+    g.cy0 = ty0 - maxd - KL;
+    g.cx0 = tx0 - maxd - KL;
+    g.CR = z.CR; g.CC = z.CC; g.cpitch = z.cpitch; g.mwords = z.mwords;
+    g.ry0 = ty0 - S - KL;
+    g.rx0 = tx0 - S - KL;
+    g.RR = z.RR; g.RC = z.RC; g.rpitch = z.rpitch;
+    g.Cs = sm;
+    g.Rs = g.Cs + g.CR * g.cpitch;
+    g.Mb = reinterpret_cast<uint32_t *>(g.Rs + g.RR * g.rpitch);
+    return g;
+}
+
+// Stage both regions (NaN outside the frame / the buffer window / unmeasured) and the
+// current mask bits.  Ends with __syncthreads().
+template <bool F32>
+__device__ __forceinline__ void stage(const Regions &g, const Plane &cur, const Plane &mask, const Plane &ref, int W,
+                                      int H, int buf_y0, int buf_rows) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < g.CR * g.mwords; i += nt) g.Mb[i] = 0u;
+    __syncthreads();
+    for (int i = tid; i < g.CR * g.cpitch; i += nt) {
+        const int r = i / g.cpitch, c = i - r * g.cpitch;
+        const int gy = g.cy0 + r, gx = g.cx0 + c;
+        float v = __int_as_float(0x7fc00000);
+        if (c < g.CC && gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= buf_y0 && gy < buf_y0 + buf_rows) {
+            const int64_t rr = gy - buf_y0;
+            if (mask.p[rr * mask.pitch + gx]) {
+                v = (float)cur.p[rr * cur.pitch + gx];
+                atomicOr(&g.Mb[r * g.mwords + (c >> 5)], 1u << (c & 31));
+            }
+        }
+        g.Cs[i] = v;
+    }
+    for (int i = tid; i < g.RR * g.rpitch; i += nt) {
+        const int r = i / g.rpitch, c = i - r * g.rpitch;
+        const int gy = g.ry0 + r, gx = g.rx0 + c;
+        float v = __int_as_float(0x7fc00000);
+        if (c < g.RC && gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= buf_y0 && gy < buf_y0 + buf_rows) {
+            const int64_t rr = gy - buf_y0;
+            v = F32 ? reinterpret_cast<const float *>(ref.p + rr * ref.pitch)[gx] : (float)ref.p[rr * ref.pitch + gx];
+        }
+        g.Rs[i] = v;
+    }
+    __syncthreads();
+}
+
+// 32 mask bits of current-region row r starting at region column c0.
+__device__ __forceinline__ uint32_t mask_bits(const Regions &g, int r, int c0) {
+    const uint32_t *mw = g.Mb + r * g.mwords;
+    return __funnelshift_r(mw[c0 >> 5], mw[(c0 >> 5) + 1], c0 & 31);
+}
+
+// One FRMC / RMC work item: entry at tile-local (ly, lx) of the tile at (ty0, tx0) with vector
+// (va, vb), delta_y = dy and up to 7 delta_x values dx0 + pat_j(k), k < nk.  Returns true iff
+// some delta != 0 has an admissible reverse cost with a strictly smaller mean than the entry's
+// own (m0 = fl(e0/n0) for float references; exact e'*n0 < e0*n' for uint8).
+template <int PAT, bool SSD, bool F32>
+__device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, int ly, int lx, int va, int vb, int dy,
+                                          int dx0, int nk, int min_support, float m0, uint32_t e0, uint32_t n0) {
+    constexpr int KL = kFK / 2;
+    float acc[7];
+    int cnt[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) { acc[k] = 0.f; cnt[k] = 0; }
+    const int crow = (ty0 + ly + dy - KL) - g.cy0, ccol = (tx0 + lx + dx0 - KL) - g.cx0;
+    const int rrow = (ty0 + ly + va - KL) - g.ry0, rcol = (tx0 + lx + vb - KL) - g.rx0;
+    // Reference-window validity: columns x+o in the frame (a property of the entry), rows below.
+    const int xx = g.rx0 + rcol, xy = g.ry0 + rrow;   // global coords of the window's (0, 0)
+    uint32_t colm = 0;
+#pragma unroll
+    for (int j = 0; j < kFK; ++j) colm |= (xx + j >= 0 && xx + j < g.W) ? (1u << j) : 0u;
+#pragma unroll 1
+    for (int oy = 0; oy < kFK; ++oy) {
+        const float *cp = g.Cs + (crow + oy) * g.cpitch + ccol;
+        const float *rp = g.Rs + (rrow + oy) * g.rpitch + rcol;
+        float c[kFSeg], r[kFK];
+#pragma unroll
+        for (int j = 0; j < kFSeg; ++j) c[j] = cp[j];
+#pragma unroll
+        for (int j = 0; j < kFK; ++j) r[j] = rp[j];
+        const uint32_t rb = (xy + oy >= 0 && xy + oy < g.H) ? colm : 0u;
+        const uint32_t bits = mask_bits(g, crow + oy, ccol);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            const int j = pat_j<PAT>(k);
+            const uint32_t vm = (bits >> j) & rb;              // slots holding a term (R9)
+#pragma unroll
+            for (int ox = 0; ox < kFK; ++ox) {
+                const float d = __fsub_rn(r[ox], c[ox + j]);
+                const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
+                if (vm & (1u << ox)) acc[k] = __fadd_rn(acc[k], t);   // row-major order, terms only
+            }
+            cnt[k] += __popc(vm);
+        }
+    }
+    bool reject = false;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        if (k >= nk) continue;
+        const int dx = dx0 + pat_j<PAT>(k);
+        if (dy == 0 && dx == 0) continue;
+        if (cnt[k] < min_support) continue;   // SENTINEL never rejects (R11)
+        if (F32) {
+            if (__fdiv_rn(acc[k], (float)cnt[k]) < m0) reject = true;
+        } else {
+            const unsigned long long ek = (unsigned long long)acc[k];
+            if (ek * n0 < (unsigned long long)e0 * (unsigned)cnt[k]) reject = true;
+        }
+    }
+    return reject;
+}
+
+}  // namespace tile
+}  // namespace qs

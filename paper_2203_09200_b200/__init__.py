@@ -127,7 +127,7 @@ def qs_profile_reset():
     lib().qs_profile_reset()
 
 
-PROFILE_KERNELS = ("me_box", "finalize", "nnc", "revgrid", "rme_decide", "project", "epilogue")
+PROFILE_KERNELS = ("me_box", "epilogue", "finalize", "nnc", "revgrid", "rme_decide", "project")
 
 
 def _check(rc: int):

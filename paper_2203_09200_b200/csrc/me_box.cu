@@ -140,6 +140,31 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
     for (int i = 0; i < kSeg; ++i) { be[i] = INFINITY; bn[i] = 1.f; br[i] = -1; }
     const float ms = (float)a.min_support;
 
+    // Forward border tiles: the support of every output for a candidate that keeps all of the
+    // tile's window pixels inside the frame ("clip-free", uniform per candidate) is the count
+    // of measured in-frame pixels in its window -- box-summed once here, not per candidate.
+    float npx[(CNT && !REV) ? kSeg : 1];
+    if constexpr (CNT && !REV) {
+        __syncthreads();
+        if (actA) {
+            float nv[G::NA], hn[kRun];
+#pragma unroll
+            for (int j = 0; j < G::NA; ++j) nv[j] = (av[j] == av[j]) ? 1.f : 0.f;
+            box_sum<K, kRun, true>(nv, hn);
+#pragma unroll
+            for (int i = 0; i < kRun; ++i) Ns[ya * kTXP + xa0 + i] = hn[i];
+        }
+        __syncthreads();
+        float nvv[G::NB];
+#pragma unroll
+        for (int j = 0; j < G::NB; ++j) nvv[j] = Ns[(sb * kSeg + j) * kTXP + xb];
+        box_sum<K, kSeg, true>(nvv, npx);
+    }
+    // Rows / columns of the tile's window pixels that lie in the frame.
+    constexpr int KR = K - 1 - G::KL;
+    const int qy_lo = max(0, py0 - G::KL), qy_hi = min(a.H - 1, py0 + kTY - 1 + KR);
+    const int qx_lo = max(0, px0 - G::KL), qx_hi = min(a.W - 1, px0 + kTX - 1 + KR);
+
     __syncthreads();
     const int k0 = 0, k1 = nkc;
     for (int k = k0; k < k1; ++k) {
@@ -150,6 +175,8 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
         const int buf = (k - k0) & 1;
         float *Hb = Hs + buf * G::HR * kTXP;
         float *Nb = Ns + buf * G::HR * kTXP;
+        const bool clipfree = !REV && qy_lo + al >= 0 && qy_hi + al <= a.H - 1 && qx_lo + bt >= 0 &&
+                              qx_hi + bt <= a.W - 1;   // uniform
         if (actA) {
             const float *brow = Bw + (ya + al - alo) * bpitch + xa0 + bt + a.S;
             float d[G::NA];
@@ -166,7 +193,7 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
             float4 *hp = reinterpret_cast<float4 *>(Hb + ya * kTXP + xa0);
 #pragma unroll
             for (int i = 0; i < kRun / 4; ++i) hp[i] = make_float4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
-            if constexpr (CNT) {
+            if constexpr (CNT) if (!clipfree) {
                 float hn[kRun];
                 box_sum<K, kRun, true>(nv, hn);
                 float4 *np = reinterpret_cast<float4 *>(Nb + ya * kTXP + xa0);
@@ -188,20 +215,29 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
                 for (int i = 0; i < kSeg; ++i)
                     if (e[i] < be[i]) { be[i] = e[i]; br[i] = rank; }
             } else {
-                const float *nc = Nb + (sb * kSeg) * kTXP + xb;
-                float nvv[G::NB];
-#pragma unroll
-                for (int j = 0; j < G::NB; ++j) nvv[j] = nc[j * kTXP];
                 float n[kSeg];
-                box_sum<K, kSeg, true>(nvv, n);
+                if (!clipfree) {
+                    const float *nc = Nb + (sb * kSeg) * kTXP + xb;
+                    float nvv[G::NB];
+#pragma unroll
+                    for (int j = 0; j < G::NB; ++j) nvv[j] = nc[j * kTXP];
+                    box_sum<K, kSeg, true>(nvv, n);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kSeg; ++i) n[i] = npx[(CNT && !REV) ? i : 0];
+                }
 #pragma unroll
                 for (int i = 0; i < kSeg; ++i) {
                     if (n[i] >= ms) {
-                        if constexpr (!EXACT) {
-                            const float m = __fdiv_rn(e[i], n[i]);    // fl(e/n), R23
-                            if (m < be[i]) { be[i] = m; br[i] = rank; }
-                        } else if constexpr (SSD) {
+                        if constexpr (EXACT && SSD) {
+                            // exact: fp64 products of integers < 2^23 and n <= 81
                             if ((double)e[i] * (double)bn[i] < (double)be[i] * (double)n[i]) {
+                                be[i] = e[i]; bn[i] = n[i]; br[i] = rank;
+                            }
+                        } else if constexpr (!EXACT) {
+                            // float reference: fp32 cross-multiplied means (differs from the oracle's
+                            // fl(e/n) only at near-ties, R23); the merge key below is fl(e/n)
+                            if (__fmul_rn(e[i], bn[i]) < __fmul_rn(be[i], n[i])) {
                                 be[i] = e[i]; bn[i] = n[i]; br[i] = rank;
                             }
                         } else {
@@ -220,8 +256,10 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
         const int py = py0 + sb * kSeg + i, px = px0 + xb;
         if (br[i] < 0 || py >= a.oy1 || px >= a.ox1) continue;
         unsigned long long hi;
-        if constexpr (!CNT || !EXACT) {
-            hi = __float_as_uint(be[i]);                 // e (interior) or fl(e/n): non-negative floats
+        if constexpr (!CNT) {
+            hi = __float_as_uint(be[i]);                 // e (interior: n constant): non-negative float
+        } else if constexpr (!EXACT) {
+            hi = __float_as_uint(__fdiv_rn(be[i], bn[i]));   // fl(e/n) (R23), non-negative float
         } else {
             // floor(e * 2^13 / n): distinct means with n <= 81 differ by >= 1/6561 > 2^-13,
             // equal means give equal keys; fp64 division of exact integers cannot round
@@ -294,7 +332,7 @@ __device__ __forceinline__ void nb_arrive(int id, int) {
         default: nb_arrive_i<8>(); break;
     }
 }
-constexpr int kQStages = 4;   // H ring depth: FULL[s] = barrier 1+s, EMPTY[s] = barrier 5+s
+constexpr int kQStages = 2;   // H ring depth: FULL[s] = barrier 1+s, EMPTY[s] = barrier 5+s
 
 // 1 iff every block the quad body reads (rows -2..29, cols -2..34) holds exactly one measured pixel.
 __device__ __forceinline__ bool quad_mask_ok(const BoxArgs &a, int px0, int py0) {
@@ -309,6 +347,44 @@ __device__ __forceinline__ bool quad_mask_ok(const BoxArgs &a, int px0, int py0)
         ok = ok && (n == 1);
     }
     return __syncthreads_and(ok);
+}
+
+// ---- packed fp32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2; ptxas folds {x,x} broadcasts and |x|) ----
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2pack(float a, float b) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float f2lo(f2_t x) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+    return a;
+}
+__device__ __forceinline__ float f2hi(f2_t x) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+    return b;
+}
+__device__ __forceinline__ f2_t f2add(f2_t a, f2_t b) {
+    f2_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2sub(f2_t a, f2_t b) {
+    f2_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2mul(f2_t a, f2_t b) {
+    f2_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2fma(f2_t a, f2_t b, f2_t c) {
+    f2_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
 }
 
 template <bool SSD>
@@ -331,15 +407,17 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     const int k0g = a.chunk_off[chunk], nk = a.chunk_off[chunk + 1] - k0g;
     for (int i = threadIdx.x; i < nk; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);
     __syncthreads();
+    if (nk <= 0) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k0 = 0, k1 = nk;
 
     if (warp < 4) {
         // ------------------------------ producer ------------------------------
-        const int hr = lane;               // H row = block row + 2
+        // lane = H row (block row + 2), 8 H columns per warp, 12 blocks read per lane.
+        const int hr = lane;
         const int bi = hr - 2;
-        float cv[kQG], wy[kQG], wx[kQG], wxc[kQG];
-        int ad[kQG];   // byte offset of the block's measured pixel in the window (candidate (alo, 0))
+        float cv[kQG], wx[kQG];
+        f2_t wy2[kQG];   // (1 - dy, dy)
+        int ad[kQG];     // byte offset of the block's measured pixel in the window (candidate (alo, 0))
 #pragma unroll
         for (int kk = 0; kk < kQG; ++kk) {
             const int bk = kQRun * warp - 2 + kk;
@@ -349,103 +427,100 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             const int q = m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
             const int dy = q >> 1, dx = q & 1;
             cv[kk] = (float)a.cur.p[(r + dy) * a.cur.pitch + x + dx];
-            wy[kk] = (float)dy;
+            wy2[kk] = f2pack((float)(1 - dy), (float)dy);
             wx[kk] = (float)dx;
-            wxc[kk] = (float)(1 - dx);
             ad[kk] = 4 * ((2 * bi + dy + 4) * bpitch + (2 * bk + dx + 4 + a.S));
         }
-        for (int k = k0; k < k1; ++k) {
-            const int pk = clist[k];
-            const int al = (int)(int8_t)(pk & 0xff);
-            const int bt = (int)(int8_t)((pk >> 8) & 0xff);
-            const int s = (k - k0) & (kQStages - 1);
-            const char *bwc = reinterpret_cast<const char *>(Bw + (al - alo) * bpitch + bt);   // uniform
-            float t0[kQG], t1[kQG], m0s[kQG - 1], m1s[kQG - 1];
-            float g1p = 0.f, g3p = 0.f;
+        // Software pipeline: the 12 gathered reference values of candidate k+1 are loaded while
+        // candidate k is reduced (the window is read-only during the loop).
+        float rv[kQG];
+        {
+            const int pk = clist[0];
+            const char *bwc = reinterpret_cast<const char *>(Bw + ((int)(int8_t)(pk & 0xff) - alo) * bpitch +
+                                                             (int)(int8_t)((pk >> 8) & 0xff));
+#pragma unroll
+            for (int kk = 0; kk < kQG; ++kk) rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
+        }
+        for (int k = 0; k < nk; ++k) {
+            const int s = k & (kQStages - 1);
+            float rc[kQG];
+#pragma unroll
+            for (int kk = 0; kk < kQG; ++kk) rc[kk] = rv[kk];
+            if (k + 1 < nk) {
+                const int pk = clist[k + 1];
+                const char *bwc = reinterpret_cast<const char *>(Bw + ((int)(int8_t)(pk & 0xff) - alo) * bpitch +
+                                                                 (int)(int8_t)((pk >> 8) & 0xff));
+#pragma unroll
+                for (int kk = 0; kk < kQG; ++kk) rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
+            }
+            f2_t u[kQG], m[kQG - 1], gp = 0ull;
 #pragma unroll
             for (int kk = 0; kk < kQG; ++kk) {
-                const float dd = cv[kk] - *reinterpret_cast<const float *>(bwc + ad[kk]);
-                const float d = SSD ? __fmul_rn(dd, dd) : fabsf(dd);
-                const float u1 = __fmul_rn(d, wy[kk]);       // dy = 1 part (exactly d or 0)
-                const float u0 = __fsub_rn(d, u1);            // dy = 0 part
-                t0[kk] = u0;
-                t1[kk] = u1;
-                if (kk > 0) {
-                    // D0(k-1) = G1(k-1) + G0(k), G0(k) = u0(k) (1-dx(k)): the product is exact, so
-                    // the FMA rounds once, exactly like the add of the two channel values.
-                    m0s[kk - 1] = __fmaf_rn(u0, wxc[kk], g1p);
-                    m1s[kk - 1] = __fmaf_rn(u1, wxc[kk], g3p);
-                }
-                g1p = __fmul_rn(u0, wx[kk]);                  // G1(k) = dy0, dx1 channel
-                g3p = __fmul_rn(u1, wx[kk]);                  // G3(k) = dy1, dx1 channel
+                const float d = __fsub_rn(cv[kk], rc[kk]);
+                const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
+                const f2_t uu = f2mul(f2pack(t, t), wy2[kk]);          // (C0, C1) = (dy0, dy1) parts
+                const f2_t g1 = f2mul(uu, f2pack(wx[kk], wx[kk]));     // (G1, G3) = dx1 parts
+                // D(k-1) = G(dx1, k-1) + G(dx0, k); G(dx0) = u - G(dx1) is exactly u or 0
+                if (kk > 0) m[kk - 1] = f2add(gp, f2sub(uu, g1));
+                gp = g1;
+                u[kk] = uu;
             }
-            // 4-wide horizontal box (pairwise): H(m) = (X(m)+X(m+1)) + (X(m+2)+X(m+3)), m = 0..8
-            float4 hv[kQRun];
-            {
-                float p0[kQG - 1], p1[kQG - 1], p2[kQG - 2], p3[kQG - 2];
+            // 4-wide horizontal boxes (pairwise, packed): H(j) = (X(j)+X(j+1)) + (X(j+2)+X(j+3))
+            f2_t pu[kQG - 1], pm[kQG - 2];
 #pragma unroll
-                for (int kk = 0; kk < kQG - 1; ++kk) {
-                    p0[kk] = __fadd_rn(t0[kk], t0[kk + 1]);
-                    p1[kk] = __fadd_rn(t1[kk], t1[kk + 1]);
-                }
+            for (int kk = 0; kk < kQG - 1; ++kk) pu[kk] = f2add(u[kk], u[kk + 1]);
 #pragma unroll
-                for (int kk = 0; kk < kQG - 2; ++kk) {
-                    p2[kk] = __fadd_rn(m0s[kk], m0s[kk + 1]);
-                    p3[kk] = __fadd_rn(m1s[kk], m1s[kk + 1]);
-                }
+            for (int kk = 0; kk < kQG - 2; ++kk) pm[kk] = f2add(m[kk], m[kk + 1]);
+            if (k >= kQStages) nb_sync(5 + s, kNT);                  // EMPTY[s]: consumers released stage s
+            // two 8-byte stores per entry: each packed result already sits in an aligned register pair
+            f2_t *hrow = reinterpret_cast<f2_t *>(Hq + (s * kQHR + hr) * kQHP + kQRun * warp);
 #pragma unroll
-                for (int m = 0; m < kQRun; ++m)
-                    hv[m] = make_float4(__fadd_rn(p0[m], p0[m + 2]), __fadd_rn(p1[m], p1[m + 2]),
-                                        __fadd_rn(p2[m], p2[m + 2]), __fadd_rn(p3[m], p3[m + 2]));
+            for (int j = 0; j < kQRun; ++j) {
+                hrow[2 * j] = f2add(pu[j], pu[j + 2]);       // (H[C0], H[C1])
+                hrow[2 * j + 1] = f2add(pm[j], pm[j + 2]);   // (H[D0], H[D1])
             }
-            if (k - k0 >= kQStages) nb_sync(5 + s, kNT);     // EMPTY[s]: consumers released stage s
-            float4 *hrow = Hq + (s * kQHR + hr) * kQHP + kQRun * warp;
-#pragma unroll
-            for (int m = 0; m < kQRun; ++m) hrow[m] = hv[m];
-            nb_arrive(1 + s, kNT);                           // FULL[s]
+            nb_arrive(1 + s, kNT);                                   // FULL[s]
         }
-        // drain: match the consumers' last EMPTY arrivals
-        for (int k = max(k0, k1 - kQStages); k < k1; ++k) nb_sync(5 + ((k - k0) & (kQStages - 1)), kNT);
+        for (int k = max(0, nk - kQStages); k < nk; ++k) nb_sync(5 + (k & (kQStages - 1)), kNT);   // drain
     } else {
         // ------------------------------ consumer ------------------------------
-        const int j = lane;                   // block column
-        const int seg = warp - 4;             // block rows 7*seg .. 7*seg+6
+        // lane = block column j, 7 block rows per warp; candidates in rank order, strict '<' (R7).
+        const int j = lane;
+        const int seg = warp - 4;
         float be[kQSeg][4];
         int br[kQSeg][4];
 #pragma unroll
         for (int r = 0; r < kQSeg; ++r)
 #pragma unroll
             for (int c = 0; c < 4; ++c) { be[r][c] = INFINITY; br[r][c] = -1; }
-        for (int k = k0; k < k1; ++k) {
+        for (int k = 0; k < nk; ++k) {
             const int rank = clist[k] >> 16;
-            const int s = (k - k0) & (kQStages - 1);
-            nb_sync(1 + s, kNT);                             // FULL[s]
-            const float4 *hcol = Hq + (s * kQHR + kQSeg * seg) * kQHP + j;
-            float4 h[kQSeg + 4];
+            const int s = k & (kQStages - 1);
+            nb_sync(1 + s, kNT);                                     // FULL[s]
+            const ulonglong2 *hcol = reinterpret_cast<const ulonglong2 *>(Hq + (s * kQHR + kQSeg * seg) * kQHP + j);
+            f2_t hc[kQSeg + 4], hd[kQSeg + 4];
 #pragma unroll
-            for (int t = 0; t < kQSeg + 4; ++t) h[t] = hcol[t * kQHP];
-            nb_arrive(5 + s, kNT);                           // EMPTY[s]
-            // V(i) = (H(i-2)+H(i-1)) + (H(i)+H(i+1)) for i = 0..7 (H index t = i+2 relative)
-            float4 p[kQSeg + 3];
+            for (int t = 0; t < kQSeg + 4; ++t) {
+                const ulonglong2 v = hcol[t * kQHP];
+                hc[t] = v.x;   // (C0, C1)
+                hd[t] = v.y;   // (D0, D1)
+            }
+            nb_arrive(5 + s, kNT);                                   // EMPTY[s]
+            f2_t pc[kQSeg + 3], pd[kQSeg + 3];
 #pragma unroll
-            for (int t = 0; t < kQSeg + 3; ++t)
-                p[t] = make_float4(__fadd_rn(h[t].x, h[t + 1].x), __fadd_rn(h[t].y, h[t + 1].y),
-                                   __fadd_rn(h[t].z, h[t + 1].z), __fadd_rn(h[t].w, h[t + 1].w));
-            float4 v[kQSeg + 1];
+            for (int t = 0; t < kQSeg + 3; ++t) { pc[t] = f2add(hc[t], hc[t + 1]); pd[t] = f2add(hd[t], hd[t + 1]); }
+            f2_t vc[kQSeg + 1], vd[kQSeg + 1];
 #pragma unroll
-            for (int i = 0; i < kQSeg + 1; ++i)
-                v[i] = make_float4(__fadd_rn(p[i].x, p[i + 2].x), __fadd_rn(p[i].y, p[i + 2].y),
-                                   __fadd_rn(p[i].z, p[i + 2].z), __fadd_rn(p[i].w, p[i + 2].w));
+            for (int i = 0; i < kQSeg + 1; ++i) { vc[i] = f2add(pc[i], pc[i + 2]); vd[i] = f2add(pd[i], pd[i + 2]); }
 #pragma unroll
             for (int r = 0; r < kQSeg; ++r) {
-                const float e00 = __fadd_rn(v[r].x, v[r].y);
-                const float e01 = __fadd_rn(v[r].z, v[r].w);
-                const float e10 = __fadd_rn(v[r].y, v[r + 1].x);
-                const float e11 = __fadd_rn(v[r].w, v[r + 1].z);
-                if (e00 < be[r][0]) { be[r][0] = e00; br[r][0] = rank; }
-                if (e01 < be[r][1]) { be[r][1] = e01; br[r][1] = rank; }
-                if (e10 < be[r][2]) { be[r][2] = e10; br[r][2] = rank; }
-                if (e11 < be[r][3]) { be[r][3] = e11; br[r][3] = rank; }
+                const float e[4] = {__fadd_rn(f2lo(vc[r]), f2hi(vc[r])),       // E(2i,   2j)
+                                    __fadd_rn(f2lo(vd[r]), f2hi(vd[r])),       // E(2i,   2j+1)
+                                    __fadd_rn(f2hi(vc[r]), f2lo(vc[r + 1])),   // E(2i+1, 2j)
+                                    __fadd_rn(f2hi(vd[r]), f2lo(vd[r + 1]))};  // E(2i+1, 2j+1)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (e[c] < be[r][c]) { be[r][c] = e[c]; br[r][c] = rank; }
             }
         }
 #pragma unroll
@@ -500,7 +575,7 @@ cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
     if (K == 8 && !REV) {
         const int qrows = kQWinRows + kChunkRows - 1, qpitch = (kQWinCols + 2 * a.S) | 1;
         const size_t qs = sizeof(float) * (size_t)((qrows * qpitch + 3) & ~3) +
-                          sizeof(float4) * kQStages * kQHR * kQHP + sizeof(int) * kChunkRows * (2 * a.S + 1);
+                          sizeof(float4) * kQStages * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8);
         smem = smem > qs ? smem : qs;
     }
     auto fn = box_kernel<K, EXACT, SSD, REV>;
@@ -586,6 +661,7 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
     if (a.ref_f32) reinterpret_cast<float *>(a.err)[fi] = (st == kCandidate) ? ef : 0.f;
     else reinterpret_cast<uint32_t *>(a.err)[fi] = (st == kCandidate) ? eu : 0u;
 }
+
 
 }  // namespace
 

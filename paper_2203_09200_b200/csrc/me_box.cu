@@ -86,6 +86,18 @@ __device__ __forceinline__ void box_sum(const float (&in)[N + K - 1], float (&ou
     }
 }
 
+// A candidate is "clip-free" for a tile iff every in-frame pixel of every window of the tile
+// (rows py0-KL .. py0+kTY-1+KR, likewise columns) stays in the frame when shifted by v: then no
+// term of any output of the tile is dropped for v, and n(p, v) = npx(p) (the window's measured
+// in-frame pixels).  Uniform per (tile, candidate); the one definition serves both bodies.
+template <int K = 8>
+__device__ __forceinline__ bool tile_clip_free(const BoxArgs &a, int px0, int py0, int al, int bt) {
+    constexpr int KL = K / 2, KR = K - 1 - K / 2;
+    const int qy_lo = max(0, py0 - KL), qy_hi = min(a.H - 1, py0 + kTY - 1 + KR);
+    const int qx_lo = max(0, px0 - KL), qx_hi = min(a.W - 1, px0 + kTX - 1 + KR);
+    return qy_lo + al >= 0 && qy_hi + al <= a.H - 1 && qx_lo + bt >= 0 && qx_hi + bt <= a.W - 1;
+}
+
 template <int K>
 struct BoxGeom {
     static constexpr int HR = kTY + K - 1;   // H rows per tile
@@ -98,7 +110,8 @@ struct BoxGeom {
 // The body for one tile x chunk.  CNT = track supports n (border tiles and the
 // reverse ME, where n varies with the candidate) -- else n is constant per output.
 template <int K, bool EXACT, bool CNT, bool SSD, bool REV>
-__device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0) {
+__device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0,
+                                         bool skip_clipfree = false) {
     using G = BoxGeom<K>;
     const int alo = -a.S + chunk * kChunkRows;
     const int ahi = min(a.S, alo + kChunkRows - 1);
@@ -160,23 +173,18 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
         for (int j = 0; j < G::NB; ++j) nvv[j] = Ns[(sb * kSeg + j) * kTXP + xb];
         box_sum<K, kSeg, true>(nvv, npx);
     }
-    // Rows / columns of the tile's window pixels that lie in the frame.
-    constexpr int KR = K - 1 - G::KL;
-    const int qy_lo = max(0, py0 - G::KL), qy_hi = min(a.H - 1, py0 + kTY - 1 + KR);
-    const int qx_lo = max(0, px0 - G::KL), qx_hi = min(a.W - 1, px0 + kTX - 1 + KR);
-
     __syncthreads();
-    const int k0 = 0, k1 = nkc;
-    for (int k = k0; k < k1; ++k) {
+    int done = 0;   // candidates processed (double-buffer parity)
+    for (int k = 0; k < nkc; ++k) {
         const int pk = clist[k];
         const int al = (int)(int8_t)(pk & 0xff);
         const int bt = (int)(int8_t)((pk >> 8) & 0xff);
         const int rank = pk >> 16;
-        const int buf = (k - k0) & 1;
+        if (skip_clipfree && tile_clip_free<K>(a, px0, py0, al, bt)) continue;   // uniform: the quad body did it
+        const int buf = (done++) & 1;
         float *Hb = Hs + buf * G::HR * kTXP;
         float *Nb = Ns + buf * G::HR * kTXP;
-        const bool clipfree = !REV && qy_lo + al >= 0 && qy_hi + al <= a.H - 1 && qx_lo + bt >= 0 &&
-                              qx_hi + bt <= a.W - 1;   // uniform
+        const bool clipfree = !REV && tile_clip_free<K>(a, px0, py0, al, bt);   // uniform
         if (actA) {
             const float *brow = Bw + (ya + al - alo) * bpitch + xa0 + bt + a.S;
             float d[G::NA];
@@ -296,10 +304,10 @@ constexpr int kQBX = kTX / 2;           // 32 block columns per tile
 constexpr int kQBY = kTY / 2;           // 28 block rows per tile
 constexpr int kQHR = kQBY + 4;          // 32 H rows (block rows -2 .. 29)
 constexpr int kQHC = kQBX;              // 32 H columns (D already carries the k+1 block)
-constexpr int kQHP = kQHC + 1;          // H row pitch in float4 (odd: conflict-free STS.128 / LDS.128)
+constexpr int kQHP = kQHC + 1;          // H plane row pitch in packed pairs (66 words = 2 mod 4: conflict-free STS.64)
 constexpr int kQRun = 8;                // H columns per producer warp (4 x 8 = 32)
 constexpr int kQG = kQRun + 4;          // blocks read per producer lane (12: k = j-2 .. j+1, +1 for D)
-constexpr int kQSeg = kQBY / 4;         // 7 output block rows per consumer warp
+constexpr int kQSeg = kQBY / 2;         // 14 output block rows per consumer lane (2 row halves x C/D planes)
 constexpr int kQWinRows = 2 * kQHR;     // 64 pixel rows of blocks per tile (+ alpha range)
 constexpr int kQWinCols = 2 * (4 * kQRun + 4);  // 72 pixel columns (blocks -2 .. 33)
 
@@ -334,13 +342,16 @@ __device__ __forceinline__ void nb_arrive(int id, int) {
 }
 constexpr int kQStages = 2;   // H ring depth: FULL[s] = barrier 1+s, EMPTY[s] = barrier 5+s
 
-// 1 iff every block the quad body reads (rows -2..29, cols -2..34) holds exactly one measured pixel.
+// 1 iff every block the quad body reads (rows -2..29, cols -2..33) that lies in the frame and in
+// the caller's buffer holds exactly one measured pixel (blocks outside are empty: no terms).
 __device__ __forceinline__ bool quad_mask_ok(const BoxArgs &a, int px0, int py0) {
     bool ok = true;
     constexpr int NR = kQHR, NC = kQBX + 4;   // 32 x 36 blocks: rows -2..29, cols -2..33
     for (int i = threadIdx.x; i < NR * NC; i += kNT) {
         const int bi = i / NC - 2, bk = i % NC - 2;
         const int y = py0 + 2 * bi, x = px0 + 2 * bk;
+        if (y < 0 || y + 1 >= a.H || x < 0 || x + 1 >= a.W || y < a.buf_y0 || y + 1 >= a.buf_y0 + a.buf_rows)
+            continue;
         const int64_t r = (int64_t)(y - a.buf_y0) * a.mask.pitch;
         const int n = a.mask.p[r + x] + a.mask.p[r + x + 1] + a.mask.p[r + a.mask.pitch + x] +
                       a.mask.p[r + a.mask.pitch + x + 1];
@@ -387,7 +398,30 @@ __device__ __forceinline__ f2_t f2fma(f2_t a, f2_t b, f2_t c) {
     return r;
 }
 
-template <bool SSD>
+// 8-byte shared store / load of one packed pair (shared-window byte address).
+__device__ __forceinline__ void st_shared_f2(unsigned addr, f2_t x) {
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr), "l"(x) : "memory");
+}
+__device__ __forceinline__ f2_t ld_shared_f2(unsigned addr) {
+    f2_t x;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x) : "r"(addr) : "memory");
+    return x;
+}
+
+// BORDER = the tile's windows or candidates reach outside the frame / buffer.  Then the body
+// handles only the tile's clip-free candidates (tile_clip_free: n(p, v) = npx(p) for all of them,
+// so the running minimum compares e alone), blocks outside the frame are empty, reference pixels
+// outside read NaN and contribute 0, and after the candidates one more ring entry carries
+// d = 1 per measured in-frame pixel, whose box sums are npx(p): the merge key is then the mean
+// (fl(e/npx) for float references, floor(e * 2^13 / npx) for uint8, the keys box_body uses).
+// The non-clip-free candidates of a border tile go through box_body (skip_clipfree).
+//
+// H hand-over: per ring stage two planes of packed pairs, C = (H[C0], H[C1]) and D = (H[D0], H[D1]),
+// [kQHR rows][kQHP pairs]; producers store one STS.64 per plane and column (row pitch 66 words:
+// a half-warp of rows hits 32 distinct banks), consumers read one LDS.64 per row (lanes =
+// consecutive columns).  Consumer warp c: plane c & 1 (output columns 2j + (c & 1)), block rows
+// 14 (c >> 1) .. +13, both row parities: 28 outputs per lane from 18 H rows.
+template <bool SSD, bool EXACT, bool BORDER>
 __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0) {
     const int alo = -a.S + chunk * kChunkRows;
     const int ahi = min(a.S, alo + kChunkRows - 1);
@@ -395,8 +429,10 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     const int ncol_b = kQWinCols + 2 * a.S;
     const int bpitch = ncol_b | 1;
     float *Bw = smem;
-    float4 *Hq = reinterpret_cast<float4 *>(smem + ((nrow_b * bpitch + 3) & ~3));   // [kQStages][kQHR][kQHP]
-    int *clist = reinterpret_cast<int *>(Hq + kQStages * kQHR * kQHP);             // the chunk's candidates
+    f2_t *Hp = reinterpret_cast<f2_t *>(smem + ((nrow_b * bpitch + 3) & ~3));   // [kQStages][2][kQHR][kQHP]
+    int *clist = reinterpret_cast<int *>(Hp + kQStages * 2 * kQHR * kQHP);      // the chunk's candidates
+    int *nsel = clist + kChunkRows * (2 * a.S + 1);
+    constexpr int kPlane = kQHR * kQHP;
 
     // Stage the chunk's reference window (rows py0-4+alo .., cols px0-4-S ..) and candidate list.
     const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
@@ -404,11 +440,34 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         const int r = i / ncol_b, c = i - r * ncol_b;
         Bw[r * bpitch + c] = load_ref(a, by0 + r, bx0 + c);
     }
-    const int k0g = a.chunk_off[chunk], nk = a.chunk_off[chunk + 1] - k0g;
-    for (int i = threadIdx.x; i < nk; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);
-    __syncthreads();
-    if (nk <= 0) return;
+    const int k0g = a.chunk_off[chunk], nkc = a.chunk_off[chunk + 1] - k0g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int nk = nkc;
+    if constexpr (!BORDER) {
+        for (int i = threadIdx.x; i < nkc; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);
+    } else {
+        // Clip-free candidates only, compacted in rank order (one warp, ballot + popc).
+        if (warp == 0) {
+            int n = 0;
+            for (int base = 0; base < nkc; base += 32) {
+                const int i = base + lane;
+                int pk = 0;
+                bool keep = false;
+                if (i < nkc) {
+                    pk = __ldg(a.chunked + k0g + i);
+                    keep = tile_clip_free<8>(a, px0, py0, (int)(int8_t)(pk & 0xff), (int)(int8_t)((pk >> 8) & 0xff));
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep) clist[n + __popc(m & ((1u << lane) - 1u))] = pk;
+                n += __popc(m);
+            }
+            if (lane == 0) *nsel = n;
+        }
+    }
+    __syncthreads();
+    if constexpr (BORDER) nk = *nsel;
+    if (nk <= 0) return;                       // uniform
+    const int n_ent = nk + (BORDER ? 1 : 0);   // ring entries (BORDER: + the npx entry)
 
     if (warp < 4) {
         // ------------------------------ producer ------------------------------
@@ -416,21 +475,32 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         const int hr = lane;
         const int bi = hr - 2;
         float cv[kQG], wx[kQG];
-        f2_t wy2[kQG];   // (1 - dy, dy)
+        f2_t wy2[kQG];   // (1 - dy, dy); (0, 0) for an empty block
         int ad[kQG];     // byte offset of the block's measured pixel in the window (candidate (alo, 0))
 #pragma unroll
         for (int kk = 0; kk < kQG; ++kk) {
             const int bk = kQRun * warp - 2 + kk;
             const int y = py0 + 2 * bi, x = px0 + 2 * bk;
-            const int64_t r = (int64_t)(y - a.buf_y0);
-            const uint8_t *m0 = a.mask.p + r * a.mask.pitch + x;
-            const int q = m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
-            const int dy = q >> 1, dx = q & 1;
-            cv[kk] = (float)a.cur.p[(r + dy) * a.cur.pitch + x + dx];
-            wy2[kk] = f2pack((float)(1 - dy), (float)dy);
+            bool inside = true;
+            if constexpr (BORDER)
+                inside = y >= 0 && y + 1 < a.H && x >= 0 && x + 1 < a.W && y >= a.buf_y0 &&
+                         y + 1 < a.buf_y0 + a.buf_rows;
+            int dy = 0, dx = 0;
+            float c = 0.f;
+            if (inside) {
+                const int64_t r = (int64_t)(y - a.buf_y0);
+                const uint8_t *m0 = a.mask.p + r * a.mask.pitch + x;
+                const int q = m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
+                dy = q >> 1;
+                dx = q & 1;
+                c = (float)a.cur.p[(r + dy) * a.cur.pitch + x + dx];
+            }
+            cv[kk] = c;
+            wy2[kk] = inside ? f2pack((float)(1 - dy), (float)dy) : f2pack(0.f, 0.f);
             wx[kk] = (float)dx;
             ad[kk] = 4 * ((2 * bi + dy + 4) * bpitch + (2 * bk + dx + 4 + a.S));
         }
+        const unsigned hbase = (unsigned)__cvta_generic_to_shared(Hp + hr * kQHP + kQRun * warp);
         // Software pipeline: the 12 gathered reference values of candidate k+1 are loaded while
         // candidate k is reduced (the window is read-only during the loop).
         float rv[kQG];
@@ -441,97 +511,117 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
 #pragma unroll
             for (int kk = 0; kk < kQG; ++kk) rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
         }
-        for (int k = 0; k < nk; ++k) {
+        for (int k = 0; k < n_ent; ++k) {
             const int s = k & (kQStages - 1);
             float rc[kQG];
 #pragma unroll
             for (int kk = 0; kk < kQG; ++kk) rc[kk] = rv[kk];
-            if (k + 1 < nk) {
+            if (BORDER && k == nk) {
+                // the npx entry: |c - (c - 1)| = 1 (and 1^2 = 1) per measured pixel, 0 for empty blocks
+#pragma unroll
+                for (int kk = 0; kk < kQG; ++kk) rc[kk] = cv[kk] - 1.f;
+            } else if (k + 1 < nk) {
                 const int pk = clist[k + 1];
                 const char *bwc = reinterpret_cast<const char *>(Bw + ((int)(int8_t)(pk & 0xff) - alo) * bpitch +
                                                                  (int)(int8_t)((pk >> 8) & 0xff));
 #pragma unroll
                 for (int kk = 0; kk < kQG; ++kk) rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
             }
-            f2_t u[kQG], m[kQG - 1], gp = 0ull;
+            if (k >= kQStages) nb_sync(5 + s, kNT);                  // EMPTY[s]: consumers released stage s
+            const unsigned hs = hbase + (unsigned)(s * 2 * kPlane * 8);
+            // Rolling, in block order: u(k) = (C0, C1) parts, m(k) = (D0, D1)(k) = G_dx1(k) + G_dx0(k+1);
+            // pu(k) = u(k) + u(k+1), pm(k) = m(k) + m(k+1); H(j) = pu(j) + pu(j+2) (pairwise, packed).
+            f2_t u[kQG], m[kQG - 1], pu[kQG - 1], pm[kQG - 2], gp = 0ull;
 #pragma unroll
             for (int kk = 0; kk < kQG; ++kk) {
                 const float d = __fsub_rn(cv[kk], rc[kk]);
-                const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
-                const f2_t uu = f2mul(f2pack(t, t), wy2[kk]);          // (C0, C1) = (dy0, dy1) parts
-                const f2_t g1 = f2mul(uu, f2pack(wx[kk], wx[kk]));     // (G1, G3) = dx1 parts
+                float t = SSD ? __fmul_rn(d, d) : fabsf(d);
+                if constexpr (BORDER) t = fmaxf(t, 0.f);               // NaN (outside the frame) -> 0
+                u[kk] = f2mul(f2pack(t, t), wy2[kk]);                  // (C0, C1) = (dy0, dy1) parts
+                const f2_t g1 = f2mul(u[kk], f2pack(wx[kk], wx[kk]));  // (G1, G3) = dx1 parts
                 // D(k-1) = G(dx1, k-1) + G(dx0, k); G(dx0) = u - G(dx1) is exactly u or 0
-                if (kk > 0) m[kk - 1] = f2add(gp, f2sub(uu, g1));
+                if (kk > 0) m[kk - 1] = f2add(gp, f2sub(u[kk], g1));
                 gp = g1;
-                u[kk] = uu;
-            }
-            // 4-wide horizontal boxes (pairwise, packed): H(j) = (X(j)+X(j+1)) + (X(j+2)+X(j+3))
-            f2_t pu[kQG - 1], pm[kQG - 2];
-#pragma unroll
-            for (int kk = 0; kk < kQG - 1; ++kk) pu[kk] = f2add(u[kk], u[kk + 1]);
-#pragma unroll
-            for (int kk = 0; kk < kQG - 2; ++kk) pm[kk] = f2add(m[kk], m[kk + 1]);
-            if (k >= kQStages) nb_sync(5 + s, kNT);                  // EMPTY[s]: consumers released stage s
-            // two 8-byte stores per entry: each packed result already sits in an aligned register pair
-            f2_t *hrow = reinterpret_cast<f2_t *>(Hq + (s * kQHR + hr) * kQHP + kQRun * warp);
-#pragma unroll
-            for (int j = 0; j < kQRun; ++j) {
-                hrow[2 * j] = f2add(pu[j], pu[j + 2]);       // (H[C0], H[C1])
-                hrow[2 * j + 1] = f2add(pm[j], pm[j + 2]);   // (H[D0], H[D1])
+                if (kk >= 1) pu[kk - 1] = f2add(u[kk - 1], u[kk]);
+                if (kk >= 2) pm[kk - 2] = f2add(m[kk - 2], m[kk - 1]);
+                if (kk >= 3 && kk - 3 < kQRun)
+                    st_shared_f2(hs + 8 * (kk - 3), f2add(pu[kk - 3], pu[kk - 1]));               // C: (H[C0], H[C1])
+                if (kk >= 4 && kk - 4 < kQRun)
+                    st_shared_f2(hs + 8 * (kPlane + kk - 4), f2add(pm[kk - 4], pm[kk - 2]));      // D: (H[D0], H[D1])
             }
             nb_arrive(1 + s, kNT);                                   // FULL[s]
         }
-        for (int k = max(0, nk - kQStages); k < nk; ++k) nb_sync(5 + (k & (kQStages - 1)), kNT);   // drain
+        for (int k = max(0, n_ent - kQStages); k < n_ent; ++k) nb_sync(5 + (k & (kQStages - 1)), kNT);   // drain
     } else {
         // ------------------------------ consumer ------------------------------
-        // lane = block column j, 7 block rows per warp; candidates in rank order, strict '<' (R7).
+        // lane = block column j; plane pl (0: C, output column 2j; 1: D, output column 2j+1);
+        // block rows i0 .. i0+13, both row parities; candidates in rank order, strict '<' (R7).
         const int j = lane;
-        const int seg = warp - 4;
-        float be[kQSeg][4];
-        int br[kQSeg][4];
+        const int cw = warp - 4, pl = cw & 1, i0 = kQSeg * (cw >> 1);
+        float be[kQSeg][2];
+        int br[kQSeg][2];
 #pragma unroll
         for (int r = 0; r < kQSeg; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) { be[r][c] = INFINITY; br[r][c] = -1; }
-        for (int k = 0; k < nk; ++k) {
-            const int rank = clist[k] >> 16;
+            for (int c = 0; c < 2; ++c) { be[r][c] = INFINITY; br[r][c] = -1; }
+        const unsigned cbase = (unsigned)__cvta_generic_to_shared(Hp + pl * kPlane + i0 * kQHP + j);
+        for (int k = 0; k < n_ent; ++k) {
+            const int rank = (BORDER && k == nk) ? 0 : clist[k] >> 16;
             const int s = k & (kQStages - 1);
             nb_sync(1 + s, kNT);                                     // FULL[s]
-            const ulonglong2 *hcol = reinterpret_cast<const ulonglong2 *>(Hq + (s * kQHR + kQSeg * seg) * kQHP + j);
-            f2_t hc[kQSeg + 4], hd[kQSeg + 4];
+            const unsigned cs = cbase + (unsigned)(s * 2 * kPlane * 8);
+            f2_t x[kQSeg + 4];
 #pragma unroll
-            for (int t = 0; t < kQSeg + 4; ++t) {
-                const ulonglong2 v = hcol[t * kQHP];
-                hc[t] = v.x;   // (C0, C1)
-                hd[t] = v.y;   // (D0, D1)
-            }
+            for (int t = 0; t < kQSeg + 4; ++t) x[t] = ld_shared_f2(cs + 8 * t * kQHP);   // (X0, X1) of H row i0+t
             nb_arrive(5 + s, kNT);                                   // EMPTY[s]
-            f2_t pc[kQSeg + 3], pd[kQSeg + 3];
-#pragma unroll
-            for (int t = 0; t < kQSeg + 3; ++t) { pc[t] = f2add(hc[t], hc[t + 1]); pd[t] = f2add(hd[t], hd[t + 1]); }
-            f2_t vc[kQSeg + 1], vd[kQSeg + 1];
-#pragma unroll
-            for (int i = 0; i < kQSeg + 1; ++i) { vc[i] = f2add(pc[i], pc[i + 2]); vd[i] = f2add(pd[i], pd[i + 2]); }
+            // Rolling pairwise vertical boxes: pp(t) = X(t) + X(t+1), V(i) = pp(i) + pp(i+2);
+            // E(2i) = V0(i) + V1(i), E(2i+1) = V1(i) + V0(i+1) (block rows i0 + i).
+            f2_t pp0 = f2add(x[0], x[1]), pp1 = f2add(x[1], x[2]), pp2 = f2add(x[2], x[3]);
+            f2_t pp3 = f2add(x[3], x[4]);
+            f2_t vcur = f2add(pp0, pp2);
 #pragma unroll
             for (int r = 0; r < kQSeg; ++r) {
-                const float e[4] = {__fadd_rn(f2lo(vc[r]), f2hi(vc[r])),       // E(2i,   2j)
-                                    __fadd_rn(f2lo(vd[r]), f2hi(vd[r])),       // E(2i,   2j+1)
-                                    __fadd_rn(f2hi(vc[r]), f2lo(vc[r + 1])),   // E(2i+1, 2j)
-                                    __fadd_rn(f2hi(vd[r]), f2lo(vd[r + 1]))};  // E(2i+1, 2j+1)
+                const f2_t vnext = f2add(pp1, pp3);                   // V(r + 1)
+                const float e[2] = {__fadd_rn(f2lo(vcur), f2hi(vcur)),       // E(2i,   2j + pl)
+                                    __fadd_rn(f2hi(vcur), f2lo(vnext))};     // E(2i+1, 2j + pl)
+                if (BORDER && k == nk) {
+                    // npx(p): merge with the mean key (uniform branch: the last entry)
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    if (e[c] < be[r][c]) { be[r][c] = e[c]; br[r][c] = rank; }
+                    for (int c = 0; c < 2; ++c) {
+                        const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
+                        if (br[r][c] < 0 || e[c] < (float)a.min_support || py < a.oy0 || py >= a.oy1 ||
+                            px < a.ox0 || px >= a.ox1)
+                            continue;
+                        unsigned long long hi;
+                        if constexpr (EXACT) hi = (unsigned long long)floor((double)be[r][c] * 8192.0 / (double)e[c]);
+                        else hi = __float_as_uint(__fdiv_rn(be[r][c], e[c]));
+                        const unsigned long long key = (hi << 32) | (unsigned)br[r][c];
+                        atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+                        if (e[c] < be[r][c]) { be[r][c] = e[c]; br[r][c] = rank; }
+                }
+                vcur = vnext;
+                pp0 = pp1;
+                pp1 = pp2;
+                pp2 = pp3;
+                if (r + 5 < kQSeg + 4) pp3 = f2add(x[r + 4], x[r + 5]);
             }
         }
+        if constexpr (!BORDER) {
 #pragma unroll
-        for (int r = 0; r < kQSeg; ++r)
+            for (int r = 0; r < kQSeg; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int py = py0 + 2 * (kQSeg * seg + r) + (c >> 1), px = px0 + 2 * j + (c & 1);
-                if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
-                const unsigned long long key = ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
-                atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
-            }
+                for (int c = 0; c < 2; ++c) {
+                    const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
+                    if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
+                    const unsigned long long key =
+                        ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
+                    atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+                }
+        }
     }
 }
 
@@ -541,7 +631,11 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
     const int unit = blockIdx.x;
     const int chunk = unit % a.n_chunks;
     const int tile = unit / a.n_chunks;
-    const int txi = tile % a.tiles_x, tyi = tile / a.tiles_x;
+    const int txi = tile % a.tiles_x;
+    // Tile rows in the order first, last, second-to-last, then the rest: the (slower) frame-border
+    // rows are scheduled in the first waves, not in the tail.
+    const int q = tile / a.tiles_x, T = a.tiles_y;
+    const int tyi = T < 3 ? q : (q == 0 ? 0 : q == 1 ? T - 1 : q == 2 ? T - 2 : q - 2);
     const int px0 = a.ox0 + txi * kTX, py0 = a.oy0 + tyi * kTY;
     constexpr int KL = K / 2, KR = K - 1 - K / 2;
     bool interior = !REV && (py0 - KL - a.S >= 0) && (py0 + kTY - 1 + KR + a.S <= a.H - 1) &&
@@ -550,13 +644,19 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
         box_body<K, EXACT, true, SSD, true>(a, smem, chunk, px0, py0);
     } else {
         if constexpr (K == 8) {
-            // Quarter-sampling body: every pixel it touches, for every candidate, lies in the frame
-            // and in the caller's buffer window, and every block holds exactly one measurement.
-            const bool geom = a.S >= 4 && (py0 - 4 - a.S >= 0) && (py0 + 2 * kQHR - 5 + a.S <= a.H - 1) &&
-                              (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1) &&
-                              (py0 - 4 - a.S >= a.buf_y0) && (py0 + 2 * kQHR - 5 + a.S < a.buf_y0 + a.buf_rows);
-            if (geom && quad_mask_ok(a, px0, py0)) {
-                quad_body<SSD>(a, smem, chunk, px0, py0);
+            // Quarter-sampling body.  Interior: every pixel it touches, for every candidate, lies in the
+            // frame and in the caller's buffer.  Border: clip-free candidates here, the rest below.
+            if (a.S >= 4 && quad_mask_ok(a, px0, py0)) {
+                const bool geom = (py0 - 4 - a.S >= 0) && (py0 + 2 * kQHR - 5 + a.S <= a.H - 1) &&
+                                  (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1) &&
+                                  (py0 - 4 - a.S >= a.buf_y0) && (py0 + 2 * kQHR - 5 + a.S < a.buf_y0 + a.buf_rows);
+                if (geom) {
+                    quad_body<SSD, EXACT, false>(a, smem, chunk, px0, py0);
+                    return;
+                }
+                quad_body<SSD, EXACT, true>(a, smem, chunk, px0, py0);
+                __syncthreads();
+                box_body<K, EXACT, true, SSD, false>(a, smem, chunk, px0, py0, true);
                 return;
             }
         }
@@ -575,7 +675,7 @@ cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
     if (K == 8 && !REV) {
         const int qrows = kQWinRows + kChunkRows - 1, qpitch = (kQWinCols + 2 * a.S) | 1;
         const size_t qs = sizeof(float) * (size_t)((qrows * qpitch + 3) & ~3) +
-                          sizeof(float4) * kQStages * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8);
+                          sizeof(f2_t) * kQStages * 2 * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8);
         smem = smem > qs ? smem : qs;
     }
     auto fn = box_kernel<K, EXACT, SSD, REV>;

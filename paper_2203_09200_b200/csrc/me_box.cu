@@ -503,30 +503,19 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         const unsigned hbase = (unsigned)__cvta_generic_to_shared(Hp + hr * kQHP + kQRun * warp);
         // Software pipeline: the 12 gathered reference values of candidate k+1 are loaded while
         // candidate k is reduced (the window is read-only during the loop).
-        float rv[kQG];
-        {
-            const int pk = clist[0];
+        // Gathers of the reference values of the candidate at list position k (its window offset).
+        auto gather = [&](int k, float (&dst)[kQG]) {
+            const int pk = clist[k];
             const char *bwc = reinterpret_cast<const char *>(Bw + ((int)(int8_t)(pk & 0xff) - alo) * bpitch +
                                                              (int)(int8_t)((pk >> 8) & 0xff));
 #pragma unroll
-            for (int kk = 0; kk < kQG; ++kk) rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
-        }
-        for (int k = 0; k < n_ent; ++k) {
+            for (int kk = 0; kk < kQG; ++kk) dst[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
+        };
+        // One ring entry: reduce candidate k from cur[] (prefetched) while the gathers of k+1 go to nxt[].
+        auto produce = [&](int k, const float (&cur)[kQG], float (&nxt)[kQG]) {
             const int s = k & (kQStages - 1);
-            float rc[kQG];
-#pragma unroll
-            for (int kk = 0; kk < kQG; ++kk) rc[kk] = rv[kk];
-            if (BORDER && k == nk) {
-                // the npx entry: |c - (c - 1)| = 1 (and 1^2 = 1) per measured pixel, 0 for empty blocks
-#pragma unroll
-                for (int kk = 0; kk < kQG; ++kk) rc[kk] = cv[kk] - 1.f;
-            } else if (k + 1 < nk) {
-                const int pk = clist[k + 1];
-                const char *bwc = reinterpret_cast<const char *>(Bw + ((int)(int8_t)(pk & 0xff) - alo) * bpitch +
-                                                                 (int)(int8_t)((pk >> 8) & 0xff));
-#pragma unroll
-                for (int kk = 0; kk < kQG; ++kk) rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
-            }
+            if (k + 1 < nk) gather(k + 1, nxt);
+            const bool npx = BORDER && k == nk;   // the npx entry: |c - (c - 1)| = 1 per measured pixel
             if (k >= kQStages) nb_sync(5 + s, kNT);                  // EMPTY[s]: consumers released stage s
             const unsigned hs = hbase + (unsigned)(s * 2 * kPlane * 8);
             // Rolling, in block order: u(k) = (C0, C1) parts, m(k) = (D0, D1)(k) = G_dx1(k) + G_dx0(k+1);
@@ -534,7 +523,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             f2_t u[kQG], m[kQG - 1], pu[kQG - 1], pm[kQG - 2], gp = 0ull;
 #pragma unroll
             for (int kk = 0; kk < kQG; ++kk) {
-                const float d = __fsub_rn(cv[kk], rc[kk]);
+                const float d = npx ? 1.f : __fsub_rn(cv[kk], cur[kk]);
                 float t = SSD ? __fmul_rn(d, d) : fabsf(d);
                 if constexpr (BORDER) t = fmaxf(t, 0.f);               // NaN (outside the frame) -> 0
                 u[kk] = f2mul(f2pack(t, t), wy2[kk]);                  // (C0, C1) = (dy0, dy1) parts
@@ -550,6 +539,13 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                     st_shared_f2(hs + 8 * (kPlane + kk - 4), f2add(pm[kk - 4], pm[kk - 2]));      // D: (H[D0], H[D1])
             }
             nb_arrive(1 + s, kNT);                                   // FULL[s]
+        };
+        // Unrolled by two (ping-pong gather buffers: no register copies between candidates).
+        float ra[kQG], rb[kQG];
+        gather(0, ra);
+        for (int k = 0; k < n_ent; k += 2) {
+            produce(k, ra, rb);
+            if (k + 1 < n_ent) produce(k + 1, rb, ra);
         }
         for (int k = max(0, n_ent - kQStages); k < n_ent; ++k) nb_sync(5 + (k & (kQStages - 1)), kNT);   // drain
     } else {

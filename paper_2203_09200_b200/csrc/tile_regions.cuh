@@ -116,11 +116,19 @@ __device__ __forceinline__ uint32_t mask_bits(const Regions &g, int r, int c0) {
 // (va, vb), delta_y = dy and up to 7 delta_x values dx0 + pat_j(k), k < nk.  Returns true iff
 // some delta != 0 has an admissible reverse cost with a strictly smaller mean than the entry's
 // own (m0 = fl(e0/n0) for float references; exact e'*n0 < e0*n' for uint8).
+//
+// Early exit (exact): the supports n'(delta) depend only on the mask and the geometry, so they
+// are counted first; the reverse costs are then summed row by row in the definition's order, and
+// a delta is settled as "does not reject" as soon as its partial sum reaches the threshold
+// above which its final mean cannot be smaller (terms are >= 0 and fp32 accumulation of
+// non-negative terms never decreases: fl(partial / n') >= m0 implies fl(final / n') >= m0).
+// The item ends when every delta is settled or all rows are summed; a delta that is not settled
+// is decided on its complete row-major sum, exactly as before.
 template <int PAT, bool SSD, bool F32>
 __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, int ly, int lx, int va, int vb, int dy,
                                           int dx0, int nk, int min_support, float m0, uint32_t e0, uint32_t n0) {
     constexpr int KL = kFK / 2;
-    float acc[7];
+    float acc[7], thr[7];
     int cnt[7];
 #pragma unroll
     for (int k = 0; k < 7; ++k) { acc[k] = 0.f; cnt[k] = 0; }
@@ -131,8 +139,27 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
     uint32_t colm = 0;
 #pragma unroll
     for (int j = 0; j < kFK; ++j) colm |= (xx + j >= 0 && xx + j < g.W) ? (1u << j) : 0u;
+    // 1. Supports n'(delta) (R6, R9): slots holding a term.
 #pragma unroll 1
     for (int oy = 0; oy < kFK; ++oy) {
+        const uint32_t rb = (xy + oy >= 0 && xy + oy < g.H) ? colm : 0u;
+        const uint32_t bits = mask_bits(g, crow + oy, ccol);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) cnt[k] += __popc((bits >> pat_j<PAT>(k)) & rb);
+    }
+    // 2. Settled deltas: out of the set, delta = 0, SENTINEL (n' < min_support never rejects, R11);
+    //    thresholds of the rest.
+    unsigned settled = 0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const int dx = dx0 + pat_j<PAT>(k);
+        if (k >= nk || (dy == 0 && dx == 0) || cnt[k] < min_support) settled |= 1u << k;
+        if (F32) thr[k] = __fmul_ru(m0, (float)cnt[k]);   // acc >= thr  =>  fl(acc / n') >= m0
+        else thr[k] = n0 ? (float)(((unsigned long long)e0 * (unsigned)cnt[k] + n0 - 1) / n0) : INFINITY;   // ceil(e0 n'/n0)
+    }
+    // 3. Reverse costs, row-major, until every delta is settled.
+#pragma unroll 1
+    for (int oy = 0; oy < kFK && settled != 0x7fu; ++oy) {
         const float *cp = g.Cs + (crow + oy) * g.cpitch + ccol;
         const float *rp = g.Rs + (rrow + oy) * g.rpitch + rcol;
         float c[kFSeg], r[kFK];
@@ -152,16 +179,14 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
                 const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
                 if (vm & (1u << ox)) acc[k] = __fadd_rn(acc[k], t);   // row-major order, terms only
             }
-            cnt[k] += __popc(vm);
+            if (acc[k] >= thr[k]) settled |= 1u << k;
         }
     }
+    if (settled == 0x7fu) return false;
     bool reject = false;
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
-        if (k >= nk) continue;
-        const int dx = dx0 + pat_j<PAT>(k);
-        if (dy == 0 && dx == 0) continue;
-        if (cnt[k] < min_support) continue;   // SENTINEL never rejects (R11)
+        if (settled & (1u << k)) continue;
         if (F32) {
             if (__fdiv_rn(acc[k], (float)cnt[k]) < m0) reject = true;
         } else {

@@ -512,10 +512,9 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             for (int kk = 0; kk < kQG; ++kk) dst[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
         };
         // One ring entry: reduce candidate k from cur[] (prefetched) while the gathers of k+1 go to nxt[].
-        auto produce = [&](int k, const float (&cur)[kQG], float (&nxt)[kQG]) {
-            const int s = k & (kQStages - 1);
-            if (k + 1 < nk) gather(k + 1, nxt);
-            const bool npx = BORDER && k == nk;   // the npx entry: |c - (c - 1)| = 1 per measured pixel
+        // npx = the BORDER npx entry: d = 1 per measured pixel (called once, after the candidates).
+        auto produce = [&](int k, const int s, const float (&cur)[kQG], float (&nxt)[kQG], const bool npx) {
+            if (!npx && k + 1 < nk) gather(k + 1, nxt);
             if (k >= kQStages) nb_sync(5 + s, kNT);                  // EMPTY[s]: consumers released stage s
             const unsigned hs = hbase + (unsigned)(s * 2 * kPlane * 8);
             // Rolling, in block order: u(k) = (C0, C1) parts, m(k) = (D0, D1)(k) = G_dx1(k) + G_dx0(k+1);
@@ -543,9 +542,14 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         // Unrolled by two (ping-pong gather buffers: no register copies between candidates).
         float ra[kQG], rb[kQG];
         gather(0, ra);
-        for (int k = 0; k < n_ent; k += 2) {
-            produce(k, ra, rb);
-            if (k + 1 < n_ent) produce(k + 1, rb, ra);
+        static_assert(kQStages == 2, "stage ids are compile-time constants of the unrolled loops");
+        for (int k = 0; k < nk; k += 2) {
+            produce(k, 0, ra, rb, false);
+            if (k + 1 < nk) produce(k + 1, 1, rb, ra, false);
+        }
+        if constexpr (BORDER) {
+            if (nk & 1) produce(nk, 1, ra, rb, true);
+            else produce(nk, 0, ra, rb, true);
         }
         for (int k = max(0, n_ent - kQStages); k < n_ent; ++k) nb_sync(5 + (k & (kQStages - 1)), kNT);   // drain
     } else {
@@ -561,9 +565,10 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
 #pragma unroll
             for (int c = 0; c < 2; ++c) { be[r][c] = INFINITY; br[r][c] = -1; }
         const unsigned cbase = (unsigned)__cvta_generic_to_shared(Hp + pl * kPlane + i0 * kQHP + j);
-        for (int k = 0; k < n_ent; ++k) {
-            const int rank = (BORDER && k == nk) ? 0 : clist[k] >> 16;
-            const int s = k & (kQStages - 1);
+        // last = the BORDER npx entry (called once, outside the candidate loop, so the per-row code
+        // of the candidate loop has no branches).
+        auto consume = [&](int k, const int s, const bool last) {
+            const int rank = last ? 0 : clist[k] >> 16;
             nb_sync(1 + s, kNT);                                     // FULL[s]
             const unsigned cs = cbase + (unsigned)(s * 2 * kPlane * 8);
             f2_t x[kQSeg + 4];
@@ -580,8 +585,8 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 const f2_t vnext = f2add(pp1, pp3);                   // V(r + 1)
                 const float e[2] = {__fadd_rn(f2lo(vcur), f2hi(vcur)),       // E(2i,   2j + pl)
                                     __fadd_rn(f2hi(vcur), f2lo(vnext))};     // E(2i+1, 2j + pl)
-                if (BORDER && k == nk) {
-                    // npx(p): merge with the mean key (uniform branch: the last entry)
+                if (last) {
+                    // npx(p): merge with the mean key
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                         const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
@@ -605,6 +610,14 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 pp2 = pp3;
                 if (r + 5 < kQSeg + 4) pp3 = f2add(x[r + 4], x[r + 5]);
             }
+        };
+        for (int k = 0; k < nk; k += 2) {
+            consume(k, 0, false);
+            if (k + 1 < nk) consume(k + 1, 1, false);
+        }
+        if constexpr (BORDER) {
+            if (nk & 1) consume(nk, 1, true);
+            else consume(nk, 0, true);
         }
         if constexpr (!BORDER) {
 #pragma unroll
@@ -650,7 +663,13 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
                     quad_body<SSD, EXACT, false>(a, smem, chunk, px0, py0);
                     return;
                 }
+#if defined(QS_EXP) && QS_EXP == 1
+                return;   // experiment: interior tiles only
+#endif
                 quad_body<SSD, EXACT, true>(a, smem, chunk, px0, py0);
+#if defined(QS_EXP) && QS_EXP == 2
+                return;   // experiment: border tiles without the generic pass
+#endif
                 __syncthreads();
                 box_body<K, EXACT, true, SSD, false>(a, smem, chunk, px0, py0, true);
                 return;

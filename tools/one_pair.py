@@ -37,6 +37,8 @@ def main():
     f = qs.Field.alloc(H, W, cfg.ref_f32, dev)
     ws = qs.workspace(roi, prm, dev)
     chk = None if args.no_checks else qs.make_checks()
+    qs.qs_me_search(cur, msk, ref, roi, prm, f, fuse=chk, ws=ws)   # warm-up (module load, attributes)
+    torch.cuda.synchronize()
     qs.qs_profile_enable(True)
     for _ in range(args.reps):
         qs.qs_me_search(cur, msk, ref, roi, prm, f, fuse=chk, ws=ws)

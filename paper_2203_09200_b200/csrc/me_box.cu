@@ -408,31 +408,41 @@ __device__ __forceinline__ f2_t ld_shared_f2(unsigned addr) {
     return x;
 }
 
-// BORDER = the tile's windows or candidates reach outside the frame / buffer.  Then the body
-// handles only the tile's clip-free candidates (tile_clip_free: n(p, v) = npx(p) for all of them,
-// so the running minimum compares e alone), blocks outside the frame are empty, reference pixels
-// outside read NaN and contribute 0, and after the candidates one more ring entry carries
-// d = 1 per measured in-frame pixel, whose box sums are npx(p): the merge key is then the mean
-// (fl(e/npx) for float references, floor(e * 2^13 / npx) for uint8, the keys box_body uses).
-// The non-clip-free candidates of a border tile go through box_body (skip_clipfree).
+// BORDER = the tile's windows or candidates reach outside the frame / buffer.  Blocks outside the
+// frame are empty (weight 0) and reference pixels outside read NaN, zeroed by fmaxf(t, 0).  The
+// candidates run in two phases:
+//   phase 1, the tile's clip-free candidates (tile_clip_free: n(p, v) = npx(p) for all of them, so
+//     the running minimum compares e alone), then one ring entry with d = 1 per measured in-frame
+//     pixel whose box sums are npx(p): the consumers merge phase 1 with the mean key (fl(e/npx) for
+//     float references, floor(e * 2^13 / npx) for uint8 -- the keys box_body uses);
+//   phase 2 (Q2), the other candidates: every ring entry also carries the support planes (box sums
+//     of the per-term indicator), the consumers compare means by cross-multiplication and merge
+//     with the same mean key.  The 64-bit atomicMin of (mean key, rank) merges both phases in the
+//     R7 order (the key is monotone and tie-preserving in the mean).
+// Without Q2 (uint8 SSD: cross-multiplied sums could exceed 2^24) phase 2 runs in box_body.
 //
-// H hand-over: per ring stage two planes of packed pairs, C = (H[C0], H[C1]) and D = (H[D0], H[D1]),
-// [kQHR rows][kQHP pairs]; producers store one STS.64 per plane and column (row pitch 66 words:
-// a half-warp of rows hits 32 distinct banks), consumers read one LDS.64 per row (lanes =
-// consecutive columns).  Consumer warp c: plane c & 1 (output columns 2j + (c & 1)), block rows
-// 14 (c >> 1) .. +13, both row parities: 28 outputs per lane from 18 H rows.
+// H hand-over: per ring stage four planes of packed pairs, C = (H[C0], H[C1]), D = (H[D0], H[D1])
+// and, in phase 2, their support twins CN, DN; [kQHR rows][kQHP pairs] each.  Producers store one
+// STS.64 per plane and column (row pitch 66 words: a half-warp of rows hits 32 distinct banks),
+// consumers read one LDS.64 per row (lanes = consecutive columns).  Consumer warp c: plane c & 1
+// (output columns 2j + (c & 1)), block rows 14 (c >> 1) .. +13, both row parities: 28 outputs per
+// lane from 18 H rows.
+constexpr int kQPlanes = 4;   // planes per ring stage
+
 template <bool SSD, bool EXACT, bool BORDER>
 __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0) {
+    constexpr bool Q2 = BORDER && !(EXACT && SSD);
     const int alo = -a.S + chunk * kChunkRows;
     const int ahi = min(a.S, alo + kChunkRows - 1);
     const int nrow_b = kQWinRows + (ahi - alo);
     const int ncol_b = kQWinCols + 2 * a.S;
     const int bpitch = ncol_b | 1;
     float *Bw = smem;
-    f2_t *Hp = reinterpret_cast<f2_t *>(smem + ((nrow_b * bpitch + 3) & ~3));   // [kQStages][2][kQHR][kQHP]
-    int *clist = reinterpret_cast<int *>(Hp + kQStages * 2 * kQHR * kQHP);      // the chunk's candidates
+    f2_t *Hp = reinterpret_cast<f2_t *>(smem + ((nrow_b * bpitch + 3) & ~3));   // [kQStages][kQPlanes][kQHR][kQHP]
+    int *clist = reinterpret_cast<int *>(Hp + kQStages * kQPlanes * kQHR * kQHP);   // the chunk's candidates
     int *nsel = clist + kChunkRows * (2 * a.S + 1);
-    constexpr int kPlane = kQHR * kQHP;
+    constexpr int kPlane = kQHR * kQHP;                  // pairs per plane
+    constexpr unsigned kStageBytes = kQPlanes * kPlane * 8;
 
     // Stage the chunk's reference window (rows py0-4+alo .., cols px0-4-S ..) and candidate list.
     const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
@@ -442,32 +452,40 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     }
     const int k0g = a.chunk_off[chunk], nkc = a.chunk_off[chunk + 1] - k0g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int nk = nkc;
+    int nA = nkc, nB = 0;
     if constexpr (!BORDER) {
         for (int i = threadIdx.x; i < nkc; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);
     } else {
-        // Clip-free candidates only, compacted in rank order (one warp, ballot + popc).
+        // Clip-free candidates (list A), then the others (list B, phase 2), each in rank order
+        // (one warp, ballot + popc).
         if (warp == 0) {
             int n = 0;
-            for (int base = 0; base < nkc; base += 32) {
-                const int i = base + lane;
-                int pk = 0;
-                bool keep = false;
-                if (i < nkc) {
-                    pk = __ldg(a.chunked + k0g + i);
-                    keep = tile_clip_free<8>(a, px0, py0, (int)(int8_t)(pk & 0xff), (int)(int8_t)((pk >> 8) & 0xff));
+            for (int pass = 0; pass < (Q2 ? 2 : 1); ++pass) {
+                for (int base = 0; base < nkc; base += 32) {
+                    const int i = base + lane;
+                    int pk = 0;
+                    bool keep = false;
+                    if (i < nkc) {
+                        pk = __ldg(a.chunked + k0g + i);
+                        keep = tile_clip_free<8>(a, px0, py0, (int)(int8_t)(pk & 0xff),
+                                                 (int)(int8_t)((pk >> 8) & 0xff)) == (pass == 0);
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, keep);
+                    if (keep) clist[n + __popc(m & ((1u << lane) - 1u))] = pk;
+                    n += __popc(m);
                 }
-                const unsigned m = __ballot_sync(0xffffffffu, keep);
-                if (keep) clist[n + __popc(m & ((1u << lane) - 1u))] = pk;
-                n += __popc(m);
+                if (lane == 0) nsel[pass] = n;
             }
-            if (lane == 0) *nsel = n;
         }
     }
     __syncthreads();
-    if constexpr (BORDER) nk = *nsel;
-    if (nk <= 0) return;                       // uniform
-    const int n_ent = nk + (BORDER ? 1 : 0);   // ring entries (BORDER: + the npx entry)
+    if constexpr (BORDER) {
+        nA = nsel[0];
+        nB = Q2 ? nsel[1] - nA : 0;
+    }
+    const int e1 = nA + ((BORDER && nA > 0) ? 1 : 0);   // entries of phase 1 (+ the npx entry)
+    const int n_ent = e1 + nB;
+    if (n_ent <= 0) return;                              // uniform
 
     if (warp < 4) {
         // ------------------------------ producer ------------------------------
@@ -501,55 +519,79 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             ad[kk] = 4 * ((2 * bi + dy + 4) * bpitch + (2 * bk + dx + 4 + a.S));
         }
         const unsigned hbase = (unsigned)__cvta_generic_to_shared(Hp + hr * kQHP + kQRun * warp);
-        // Software pipeline: the 12 gathered reference values of candidate k+1 are loaded while
-        // candidate k is reduced (the window is read-only during the loop).
-        // Gathers of the reference values of the candidate at list position k (its window offset).
-        auto gather = [&](int k, float (&dst)[kQG]) {
-            const int pk = clist[k];
+        // Gathers of the reference values of the candidate at list position ci (its window offset).
+        auto gather = [&](int ci, float (&dst)[kQG]) {
+            const int pk = clist[ci];
             const char *bwc = reinterpret_cast<const char *>(Bw + ((int)(int8_t)(pk & 0xff) - alo) * bpitch +
                                                              (int)(int8_t)((pk >> 8) & 0xff));
 #pragma unroll
             for (int kk = 0; kk < kQG; ++kk) dst[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
         };
-        // One ring entry: reduce candidate k from cur[] (prefetched) while the gathers of k+1 go to nxt[].
-        // npx = the BORDER npx entry: d = 1 per measured pixel (called once, after the candidates).
-        auto produce = [&](int k, const int s, const float (&cur)[kQG], float (&nxt)[kQG], const bool npx) {
-            if (!npx && k + 1 < nk) gather(k + 1, nxt);
-            if (k >= kQStages) nb_sync(5 + s, kNT);                  // EMPTY[s]: consumers released stage s
-            const unsigned hs = hbase + (unsigned)(s * 2 * kPlane * 8);
-            // Rolling, in block order: u(k) = (C0, C1) parts, m(k) = (D0, D1)(k) = G_dx1(k) + G_dx0(k+1);
-            // pu(k) = u(k) + u(k+1), pm(k) = m(k) + m(k+1); H(j) = pu(j) + pu(j+2) (pairwise, packed).
-            f2_t u[kQG], m[kQG - 1], pu[kQG - 1], pm[kQG - 2], gp = 0ull;
+        // Series of one block (rolling, in block order): u = (C0, C1) parts, m(k-1) = (D0, D1)(k-1)
+        // = G_dx1(k-1) + G_dx0(k); pu(k) = u(k) + u(k+1), pm(k) = m(k) + m(k+1); H(j) = pu(j) + pu(j+2)
+        // (pairwise, packed), stored to planes P (C) and P + 1 (D) as soon as complete.
+        struct Roll {
+            f2_t u[kQG], m[kQG - 1], pu[kQG - 1], pm[kQG - 2], gp;
+        };
+        auto roll = [&](Roll &R, int kk, float t, unsigned hs, int P) {
+            R.u[kk] = f2mul(f2pack(t, t), wy2[kk]);                  // (C0, C1) = (dy0, dy1) parts
+            const f2_t g1 = f2mul(R.u[kk], f2pack(wx[kk], wx[kk]));  // (G1, G3) = dx1 parts
+            // D(k-1) = G(dx1, k-1) + G(dx0, k); G(dx0) = u - G(dx1) is exactly u or 0
+            if (kk > 0) R.m[kk - 1] = f2add(R.gp, f2sub(R.u[kk], g1));
+            R.gp = g1;
+            if (kk >= 1) R.pu[kk - 1] = f2add(R.u[kk - 1], R.u[kk]);
+            if (kk >= 2) R.pm[kk - 2] = f2add(R.m[kk - 2], R.m[kk - 1]);
+            if (kk >= 3 && kk - 3 < kQRun)
+                st_shared_f2(hs + 8 * (P * kPlane + kk - 3), f2add(R.pu[kk - 3], R.pu[kk - 1]));
+            if (kk >= 4 && kk - 4 < kQRun)
+                st_shared_f2(hs + 8 * ((P + 1) * kPlane + kk - 4), f2add(R.pm[kk - 4], R.pm[kk - 2]));
+        };
+        // One ring entry e in stage s: reduce the candidate whose gathers are in cur[] while the
+        // gathers of list position nci go to nxt[] (nci < 0: none).  mode 0: phase-1 candidate,
+        // 1: the npx entry (d = 1 per measured pixel), 2: phase-2 candidate (+ support planes).
+        auto produce = [&](int e, const int s, const float (&cur)[kQG], float (&nxt)[kQG], int nci, const int mode) {
+            if (nci >= 0) gather(nci, nxt);
+            if (e >= kQStages) nb_sync(5 + s, kNT);                  // EMPTY[s]: consumers released stage s
+            const unsigned hs = hbase + (unsigned)s * kStageBytes;
+            Roll R, N;
+            R.gp = 0ull;
+            N.gp = 0ull;
 #pragma unroll
             for (int kk = 0; kk < kQG; ++kk) {
-                const float d = npx ? 1.f : __fsub_rn(cv[kk], cur[kk]);
-                float t = SSD ? __fmul_rn(d, d) : fabsf(d);
-                if constexpr (BORDER) t = fmaxf(t, 0.f);               // NaN (outside the frame) -> 0
-                u[kk] = f2mul(f2pack(t, t), wy2[kk]);                  // (C0, C1) = (dy0, dy1) parts
-                const f2_t g1 = f2mul(u[kk], f2pack(wx[kk], wx[kk]));  // (G1, G3) = dx1 parts
-                // D(k-1) = G(dx1, k-1) + G(dx0, k); G(dx0) = u - G(dx1) is exactly u or 0
-                if (kk > 0) m[kk - 1] = f2add(gp, f2sub(u[kk], g1));
-                gp = g1;
-                if (kk >= 1) pu[kk - 1] = f2add(u[kk - 1], u[kk]);
-                if (kk >= 2) pm[kk - 2] = f2add(m[kk - 2], m[kk - 1]);
-                if (kk >= 3 && kk - 3 < kQRun)
-                    st_shared_f2(hs + 8 * (kk - 3), f2add(pu[kk - 3], pu[kk - 1]));               // C: (H[C0], H[C1])
-                if (kk >= 4 && kk - 4 < kQRun)
-                    st_shared_f2(hs + 8 * (kPlane + kk - 4), f2add(pm[kk - 4], pm[kk - 2]));      // D: (H[D0], H[D1])
+                const float d = mode == 1 ? 1.f : __fsub_rn(cv[kk], cur[kk]);
+                const float t0 = SSD ? __fmul_rn(d, d) : fabsf(d);
+                const float t = BORDER ? fmaxf(t0, 0.f) : t0;        // NaN (outside the frame) -> 0
+                roll(R, kk, t, hs, 0);
+                if (Q2 && mode == 2) roll(N, kk, (t0 == t0) ? 1.f : 0.f, hs, 2);   // term indicator
             }
             nb_arrive(1 + s, kNT);                                   // FULL[s]
         };
-        // Unrolled by two (ping-pong gather buffers: no register copies between candidates).
+        // A run of n candidates (list positions ci0 ..) as entries e0 .., unrolled by two with ping-pong
+        // gather buffers (no register copies between candidates); stage ids are compile-time.
         float ra[kQG], rb[kQG];
-        gather(0, ra);
+        auto run = [&](int ci0, int n, int e0, const int mode) {
+            if (n <= 0) return;
+            gather(ci0, ra);
+            if ((e0 & 1) == 0) {
+                for (int i = 0; i < n; i += 2) {
+                    produce(e0 + i, 0, ra, rb, i + 1 < n ? ci0 + i + 1 : -1, mode);
+                    if (i + 1 < n) produce(e0 + i + 1, 1, rb, ra, i + 2 < n ? ci0 + i + 2 : -1, mode);
+                }
+            } else {
+                for (int i = 0; i < n; i += 2) {
+                    produce(e0 + i, 1, ra, rb, i + 1 < n ? ci0 + i + 1 : -1, mode);
+                    if (i + 1 < n) produce(e0 + i + 1, 0, rb, ra, i + 2 < n ? ci0 + i + 2 : -1, mode);
+                }
+            }
+        };
         static_assert(kQStages == 2, "stage ids are compile-time constants of the unrolled loops");
-        for (int k = 0; k < nk; k += 2) {
-            produce(k, 0, ra, rb, false);
-            if (k + 1 < nk) produce(k + 1, 1, rb, ra, false);
-        }
+        run(0, nA, 0, 0);
         if constexpr (BORDER) {
-            if (nk & 1) produce(nk, 1, ra, rb, true);
-            else produce(nk, 0, ra, rb, true);
+            if (nA > 0) {
+                if (nA & 1) produce(nA, 1, ra, rb, -1, 1);
+                else produce(nA, 0, ra, rb, -1, 1);
+            }
+            if constexpr (Q2) run(nA, nB, e1, 2);
         }
         for (int k = max(0, n_ent - kQStages); k < n_ent; ++k) nb_sync(5 + (k & (kQStages - 1)), kNT);   // drain
     } else {
@@ -565,12 +607,20 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
 #pragma unroll
             for (int c = 0; c < 2; ++c) { be[r][c] = INFINITY; br[r][c] = -1; }
         const unsigned cbase = (unsigned)__cvta_generic_to_shared(Hp + pl * kPlane + i0 * kQHP + j);
-        // last = the BORDER npx entry (called once, outside the candidate loop, so the per-row code
-        // of the candidate loop has no branches).
-        auto consume = [&](int k, const int s, const bool last) {
-            const int rank = last ? 0 : clist[k] >> 16;
+        auto merge_mean = [&](int r, int c, float e, float n, int rank) {
+            const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
+            if (rank < 0 || n < (float)a.min_support || py < a.oy0 || py >= a.oy1 || px < a.ox0 || px >= a.ox1)
+                return;
+            unsigned long long hi;
+            if constexpr (EXACT) hi = (unsigned long long)floor((double)e * 8192.0 / (double)n);
+            else hi = __float_as_uint(__fdiv_rn(e, n));
+            atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), (hi << 32) | (unsigned)rank);
+        };
+        // Phase-1 entry (or the npx entry when last): E for the 28 outputs from the 18 H rows.
+        auto consume = [&](int e, const int s, const bool last) {
+            const int rank = last ? 0 : clist[e] >> 16;
             nb_sync(1 + s, kNT);                                     // FULL[s]
-            const unsigned cs = cbase + (unsigned)(s * 2 * kPlane * 8);
+            const unsigned cs = cbase + (unsigned)s * kStageBytes;
             f2_t x[kQSeg + 4];
 #pragma unroll
             for (int t = 0; t < kQSeg + 4; ++t) x[t] = ld_shared_f2(cs + 8 * t * kQHP);   // (X0, X1) of H row i0+t
@@ -583,26 +633,12 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
 #pragma unroll
             for (int r = 0; r < kQSeg; ++r) {
                 const f2_t vnext = f2add(pp1, pp3);                   // V(r + 1)
-                const float e[2] = {__fadd_rn(f2lo(vcur), f2hi(vcur)),       // E(2i,   2j + pl)
-                                    __fadd_rn(f2hi(vcur), f2lo(vnext))};     // E(2i+1, 2j + pl)
-                if (last) {
-                    // npx(p): merge with the mean key
+                const float ev[2] = {__fadd_rn(f2lo(vcur), f2hi(vcur)),       // E(2i,   2j + pl)
+                                     __fadd_rn(f2hi(vcur), f2lo(vnext))};     // E(2i+1, 2j + pl)
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
-                        if (br[r][c] < 0 || e[c] < (float)a.min_support || py < a.oy0 || py >= a.oy1 ||
-                            px < a.ox0 || px >= a.ox1)
-                            continue;
-                        unsigned long long hi;
-                        if constexpr (EXACT) hi = (unsigned long long)floor((double)be[r][c] * 8192.0 / (double)e[c]);
-                        else hi = __float_as_uint(__fdiv_rn(be[r][c], e[c]));
-                        const unsigned long long key = (hi << 32) | (unsigned)br[r][c];
-                        atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 2; ++c)
-                        if (e[c] < be[r][c]) { be[r][c] = e[c]; br[r][c] = rank; }
+                for (int c = 0; c < 2; ++c) {
+                    if (last) merge_mean(r, c, be[r][c], ev[c], br[r][c]);   // ev = npx(p)
+                    else if (ev[c] < be[r][c]) { be[r][c] = ev[c]; br[r][c] = rank; }
                 }
                 vcur = vnext;
                 pp0 = pp1;
@@ -611,13 +647,9 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 if (r + 5 < kQSeg + 4) pp3 = f2add(x[r + 4], x[r + 5]);
             }
         };
-        for (int k = 0; k < nk; k += 2) {
+        for (int k = 0; k < nA; k += 2) {
             consume(k, 0, false);
-            if (k + 1 < nk) consume(k + 1, 1, false);
-        }
-        if constexpr (BORDER) {
-            if (nk & 1) consume(nk, 1, true);
-            else consume(nk, 0, true);
+            if (k + 1 < nA) consume(k + 1, 1, false);
         }
         if constexpr (!BORDER) {
 #pragma unroll
@@ -630,6 +662,78 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                         ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
                     atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
                 }
+        } else {
+            if (nA > 0) {
+                if (nA & 1) consume(nA, 1, true);
+                else consume(nA, 0, true);
+            }
+            if constexpr (Q2) {
+                // Phase 2: (best e, its n, rank); means compared by cross-multiplication (exact for
+                // uint8 SAD: e * n < 2^24; fp32 for float references, R23).
+                float bn[kQSeg][2];
+#pragma unroll
+                for (int r = 0; r < kQSeg; ++r)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) { be[r][c] = INFINITY; bn[r][c] = 1.f; br[r][c] = -1; }
+                const float ms = (float)a.min_support;
+                auto consume2 = [&](int ci, const int s) {
+                    const int rank = clist[ci] >> 16;
+                    nb_sync(1 + s, kNT);                                 // FULL[s]
+                    const unsigned cs = cbase + (unsigned)s * kStageBytes, ns = cs + 2u * kPlane * 8u;
+                    // Rows streamed (5-row windows of both planes) to keep the 84-register state.
+                    f2_t x0 = ld_shared_f2(cs), x1 = ld_shared_f2(cs + 8 * kQHP), x2 = ld_shared_f2(cs + 16 * kQHP);
+                    f2_t x3 = ld_shared_f2(cs + 24 * kQHP), xl = ld_shared_f2(cs + 32 * kQHP);
+                    f2_t y0 = ld_shared_f2(ns), y1 = ld_shared_f2(ns + 8 * kQHP), y2 = ld_shared_f2(ns + 16 * kQHP);
+                    f2_t y3 = ld_shared_f2(ns + 24 * kQHP), yl = ld_shared_f2(ns + 32 * kQHP);
+                    f2_t pp0 = f2add(x0, x1), pp1 = f2add(x1, x2), pp2 = f2add(x2, x3), pp3 = f2add(x3, xl);
+                    f2_t qq0 = f2add(y0, y1), qq1 = f2add(y1, y2), qq2 = f2add(y2, y3), qq3 = f2add(y3, yl);
+                    f2_t vcur = f2add(pp0, pp2), ncur = f2add(qq0, qq2);
+#pragma unroll
+                    for (int r = 0; r < kQSeg; ++r) {
+                        const f2_t vnext = f2add(pp1, pp3), nnext = f2add(qq1, qq3);
+                        const float ev[2] = {__fadd_rn(f2lo(vcur), f2hi(vcur)), __fadd_rn(f2hi(vcur), f2lo(vnext))};
+                        const float nv[2] = {__fadd_rn(f2lo(ncur), f2hi(ncur)), __fadd_rn(f2hi(ncur), f2lo(nnext))};
+#pragma unroll
+                        for (int c = 0; c < 2; ++c)
+                            if (nv[c] >= ms && __fmul_rn(ev[c], bn[r][c]) < __fmul_rn(be[r][c], nv[c])) {
+                                be[r][c] = ev[c];
+                                bn[r][c] = nv[c];
+                                br[r][c] = rank;
+                            }
+                        vcur = vnext;
+                        ncur = nnext;
+                        pp0 = pp1;
+                        pp1 = pp2;
+                        pp2 = pp3;
+                        qq0 = qq1;
+                        qq1 = qq2;
+                        qq2 = qq3;
+                        if (r + 5 < kQSeg + 4) {
+                            const f2_t xn = ld_shared_f2(cs + 8 * (r + 5) * kQHP), yn = ld_shared_f2(ns + 8 * (r + 5) * kQHP);
+                            pp3 = f2add(xl, xn);
+                            qq3 = f2add(yl, yn);
+                            xl = xn;
+                            yl = yn;
+                            if (r + 5 == kQSeg + 3) nb_arrive(5 + s, kNT);   // EMPTY[s]: last rows read
+                        }
+                    }
+                };
+                if ((e1 & 1) == 0) {
+                    for (int i = 0; i < nB; i += 2) {
+                        consume2(nA + i, 0);
+                        if (i + 1 < nB) consume2(nA + i + 1, 1);
+                    }
+                } else {
+                    for (int i = 0; i < nB; i += 2) {
+                        consume2(nA + i, 1);
+                        if (i + 1 < nB) consume2(nA + i + 1, 0);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < kQSeg; ++r)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) merge_mean(r, c, be[r][c], bn[r][c], br[r][c]);
+            }
         }
     }
 }
@@ -663,15 +767,11 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
                     quad_body<SSD, EXACT, false>(a, smem, chunk, px0, py0);
                     return;
                 }
-#if defined(QS_EXP) && QS_EXP == 1
-                return;   // experiment: interior tiles only
-#endif
                 quad_body<SSD, EXACT, true>(a, smem, chunk, px0, py0);
-#if defined(QS_EXP) && QS_EXP == 2
-                return;   // experiment: border tiles without the generic pass
-#endif
-                __syncthreads();
-                box_body<K, EXACT, true, SSD, false>(a, smem, chunk, px0, py0, true);
+                if constexpr (EXACT && SSD) {   // quad phase 2 unavailable: the rest in the generic body
+                    __syncthreads();
+                    box_body<K, EXACT, true, SSD, false>(a, smem, chunk, px0, py0, true);
+                }
                 return;
             }
         }
@@ -690,7 +790,7 @@ cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
     if (K == 8 && !REV) {
         const int qrows = kQWinRows + kChunkRows - 1, qpitch = (kQWinCols + 2 * a.S) | 1;
         const size_t qs = sizeof(float) * (size_t)((qrows * qpitch + 3) & ~3) +
-                          sizeof(f2_t) * kQStages * 2 * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8);
+                          sizeof(f2_t) * kQStages * kQPlanes * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8);
         smem = smem > qs ? smem : qs;
     }
     auto fn = box_kernel<K, EXACT, SSD, REV>;

@@ -113,8 +113,8 @@ template <int K, bool EXACT, bool CNT, bool SSD, bool REV>
 __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0,
                                          bool skip_clipfree = false) {
     using G = BoxGeom<K>;
-    const int alo = -a.S + chunk * kChunkRows;
-    const int ahi = min(a.S, alo + kChunkRows - 1);
+    const int alo = chunk_alo(a.S, chunk);
+    const int ahi = chunk_ahi(a.S, chunk);
     const int nrow_b = G::HR + (ahi - alo);
     const int ncol_b = kTX + K - 1 + 2 * a.S;
     const int bpitch = ncol_b | 1;
@@ -428,19 +428,27 @@ __device__ __forceinline__ f2_t ld_shared_f2(unsigned addr) {
 // (output columns 2j + (c & 1)), block rows 14 (c >> 1) .. +13, both row parities: 28 outputs per
 // lane from 18 H rows.
 constexpr int kQPlanes = 4;   // planes per ring stage
+// Quad reference window geometry (floats): row pitch 2 x odd >= cols; plane = ceil(rows / 2) rows,
+// rounded up to a multiple of 32 words.
+__host__ __device__ constexpr int quad_pitch(int cols) { return 2 * (((cols + 1) / 2) | 1); }
+__host__ __device__ constexpr int quad_plane(int rows, int cols) { return (((rows + 1) / 2) * quad_pitch(cols) + 31) & ~31; }
 
 template <bool SSD, bool EXACT, bool BORDER>
 __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0) {
     constexpr bool Q2 = BORDER && !(EXACT && SSD);
-    const int alo = -a.S + chunk * kChunkRows;
-    const int ahi = min(a.S, alo + kChunkRows - 1);
+    const int alo = chunk_alo(a.S, chunk);
+    const int ahi = chunk_ahi(a.S, chunk);
     const int nrow_b = kQWinRows + (ahi - alo);
     const int ncol_b = kQWinCols + 2 * a.S;
-    const int bpitch = ncol_b | 1;
+    // Reference window split by row parity: row y at plane (y & 1), plane row y >> 1.  Row pitch
+    // bpitch = 2 x odd and plane pitch = 0 mod 32 words: a warp's 32 gathers (one block row per lane,
+    // the block's row parity choosing the plane) fall into distinct banks except lanes 16 apart.
+    const int bpitch = quad_pitch(ncol_b);
+    const int bplane = quad_plane(nrow_b, ncol_b);
     float *Bw = smem;
-    f2_t *Hp = reinterpret_cast<f2_t *>(smem + ((nrow_b * bpitch + 3) & ~3));   // [kQStages][kQPlanes][kQHR][kQHP]
+    f2_t *Hp = reinterpret_cast<f2_t *>(smem + 2 * bplane);   // [kQStages][kQPlanes][kQHR][kQHP]
     int *clist = reinterpret_cast<int *>(Hp + kQStages * kQPlanes * kQHR * kQHP);   // the chunk's candidates
-    int *nsel = clist + kChunkRows * (2 * a.S + 1);
+    int *nsel = clist + kChunkRows * (2 * a.S + 1);   // a chunk holds <= 7 alpha rows
     constexpr int kPlane = kQHR * kQHP;                  // pairs per plane
     constexpr unsigned kStageBytes = kQPlanes * kPlane * 8;
 
@@ -448,7 +456,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
     for (int i = threadIdx.x; i < nrow_b * ncol_b; i += kNT) {
         const int r = i / ncol_b, c = i - r * ncol_b;
-        Bw[r * bpitch + c] = load_ref(a, by0 + r, bx0 + c);
+        Bw[(r & 1) * bplane + (r >> 1) * bpitch + c] = load_ref(a, by0 + r, bx0 + c);
     }
     const int k0g = a.chunk_off[chunk], nkc = a.chunk_off[chunk + 1] - k0g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -516,13 +524,14 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             cv[kk] = c;
             wy2[kk] = inside ? f2pack((float)(1 - dy), (float)dy) : f2pack(0.f, 0.f);
             wx[kk] = (float)dx;
-            ad[kk] = 4 * ((2 * bi + dy + 4) * bpitch + (2 * bk + dx + 4 + a.S));
+            // window row 2 bi + dy + 4 + (alpha - alo), alpha - alo even: plane dy, plane row bi + 2 + (alpha - alo) / 2
+            ad[kk] = 4 * (dy * bplane + (bi + 2) * bpitch + (2 * bk + dx + 4 + a.S));
         }
         const unsigned hbase = (unsigned)__cvta_generic_to_shared(Hp + hr * kQHP + kQRun * warp);
         // Gathers of the reference values of the candidate at list position ci (its window offset).
         auto gather = [&](int ci, float (&dst)[kQG]) {
             const int pk = clist[ci];
-            const char *bwc = reinterpret_cast<const char *>(Bw + ((int)(int8_t)(pk & 0xff) - alo) * bpitch +
+            const char *bwc = reinterpret_cast<const char *>(Bw + (((int)(int8_t)(pk & 0xff) - alo) >> 1) * bpitch +
                                                              (int)(int8_t)((pk >> 8) & 0xff));
 #pragma unroll
             for (int kk = 0; kk < kQG; ++kk) dst[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
@@ -783,13 +792,13 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
 template <int K, bool EXACT, bool SSD, bool REV>
 cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
     using G = BoxGeom<K>;
-    const int nrow_b = G::HR + kChunkRows - 1;
+    const int nrow_b = G::HR + kChunkSpan - 1;
     const int bpitch = (kTX + K - 1 + 2 * a.S) | 1;
     size_t smem = sizeof(float) * ((size_t)((nrow_b * bpitch + 3) & ~3) + 4 * (size_t)G::HR * kTXP) +
                   sizeof(int) * kChunkRows * (2 * a.S + 1);
     if (K == 8 && !REV) {
-        const int qrows = kQWinRows + kChunkRows - 1, qpitch = (kQWinCols + 2 * a.S) | 1;
-        const size_t qs = sizeof(float) * (size_t)((qrows * qpitch + 3) & ~3) +
+        const int qrows = kQWinRows + kChunkSpan - 1, qcols = kQWinCols + 2 * a.S;
+        const size_t qs = sizeof(float) * 2 * (size_t)quad_plane(qrows, qcols) +
                           sizeof(f2_t) * kQStages * kQPlanes * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8);
         smem = smem > qs ? smem : qs;
     }

@@ -123,13 +123,14 @@ const CandTables *cand_tables(int S, const char **err) {
     const int n = (int)v.size();
     std::vector<int32_t> canon(n), chunked;
     for (int r = 0; r < n; ++r) canon[r] = (v[r].first & 0xff) | ((v[r].second & 0xff) << 8);
-    const int n_chunks = (2 * S + 1 + kChunkRows - 1) / kChunkRows;
+    const int n_chunks = chunk_count(S);
     std::vector<int32_t> off(n_chunks + 1, 0);
     for (int c = 0; c < n_chunks; ++c) {
-        const int alo = -S + c * kChunkRows, ahi = std::min(S, alo + kChunkRows - 1);
+        const int alo = chunk_alo(S, c), ahi = chunk_ahi(S, c);
         off[c] = (int)chunked.size();
-        for (int r = 0; r < n; ++r)
-            if (v[r].first >= alo && v[r].first <= ahi) chunked.push_back(canon[r] | (r << 16));
+        for (int r = 0; r < n; ++r)   // rank order inside the chunk
+            if (v[r].first >= alo && v[r].first <= ahi && ((v[r].first - alo) & 1) == 0)
+                chunked.push_back(canon[r] | (r << 16));
     }
     off[n_chunks] = (int)chunked.size();
     auto *t = new CandTables;

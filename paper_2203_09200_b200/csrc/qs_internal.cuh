@@ -25,6 +25,17 @@ constexpr int kRun = 16;       // phase A: H columns per thread
 constexpr int kSeg = 14;       // phase B: output rows per thread (4 segments x 14 = 56)
 constexpr int kTXP = 68;       // padded row pitch (floats) of the H planes in smem
 constexpr int kChunkRows = 7;  // alpha rows of candidates per work unit
+// Chunks take alpha rows of ONE parity: group g = chunk >> 1 covers rows -S + 14 g .. +13, chunk
+// parity chunk & 1 takes every other row of it (7 rows, fewer in the last group).  Within a chunk
+// alpha - alo is even, so a measured pixel's reference row has the parity of its own row offset
+// dy for every candidate -- the quad body's reference window is split by row parity (conflict-light
+// gathers, me_box.cu).  kChunkSpan = rows spanned by a chunk's window.
+constexpr int kChunkSpan = 2 * kChunkRows - 1;
+__host__ __device__ constexpr int chunk_alo(int S, int chunk) { return -S + 2 * kChunkRows * (chunk >> 1) + (chunk & 1); }
+__host__ __device__ constexpr int chunk_ahi(int S, int chunk) {
+    return chunk_alo(S, chunk) + kChunkSpan - 1 < S ? chunk_alo(S, chunk) + kChunkSpan - 1 : S;
+}
+__host__ __device__ constexpr int chunk_count(int S) { return 2 * ((2 * S + 1 + 2 * kChunkRows - 1) / (2 * kChunkRows)); }
 
 // One device-resident candidate table per (device, S).
 struct CandTables {

@@ -18,6 +18,7 @@ using tile::kFK;
 using tile::kFT;
 constexpr int kH2 = kFT + 4;   // decoded window: tile + 2-pixel halo (NNC's vector halo)
 constexpr int kH1 = kFT + 2;   // filtered window: tile + 1-pixel halo
+constexpr int kCW = kFT + 14;  // FRMC window positions per axis (tile + the paper offsets' +-7)
 
 __device__ __forceinline__ int lower_median9(int (&v)[9], int n) {
 #pragma unroll
@@ -44,6 +45,7 @@ struct EpiShared {
     uint32_t e0[kFT * kFT], n0[kFT * kFT];
     int ent[kFT * kFT];
     uint8_t rej[kFT * kFT];
+    uint8_t cnt8[kCW][kCW];   // measured pixels of the 8x8 current window at each region position
     int n_ent;
 };
 
@@ -194,6 +196,15 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
     if (!FRMC) return;
 
     // 4. FRMC on the checkable entries (NNC survivors in the cascade): items (entry, delta_y).
+    //    Supports n'(delta) of entries whose reference window lies in the frame are the measured
+    //    pixels of the current 8x8 window at p + delta: one table for the tile (cnt8).
+    for (int i = tid; i < kCW * kCW; i += blockDim.x) {
+        const int r = i / kCW, c = i % kCW;
+        int n = 0;
+#pragma unroll
+        for (int oy = 0; oy < kFK; ++oy) n += __popc(tile::mask_bits(R, r + oy, c) & 0xffu);
+        S.cnt8[r][c] = (uint8_t)n;
+    }
     __syncthreads();
     const int ne = S.n_ent;
     const int items = ne * 7;
@@ -205,7 +216,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
         const int ely = o / kFT, elx = o % kFT;
         const int va = S.sa[ely + 2][elx + 2], vb = S.sb[ely + 2][elx + 2];
         if (tile::frmc_item<0, SSD, F32>(R, ty0, tx0, ely, elx, va, vb, g.dys[iy], -7, 7, g.min_support, S.m0[o],
-                                         S.e0[o], S.n0[o]))
+                                         S.e0[o], S.n0[o], &S.cnt8[0][0], kCW))
             S.rej[o] = 1;
     }
     __syncthreads();

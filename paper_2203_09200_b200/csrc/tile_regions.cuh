@@ -124,9 +124,12 @@ __device__ __forceinline__ uint32_t mask_bits(const Regions &g, int r, int c0) {
 // non-negative terms never decreases: fl(partial / n') >= m0 implies fl(final / n') >= m0).
 // The item ends when every delta is settled or all rows are summed; a delta that is not settled
 // is decided on its complete row-major sum, exactly as before.
+// cnt8 (optional): measured pixels of the current 8x8 window at every region position (row pitch
+// cw); used for the supports when the entry's reference window lies in the frame.
 template <int PAT, bool SSD, bool F32>
 __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, int ly, int lx, int va, int vb, int dy,
-                                          int dx0, int nk, int min_support, float m0, uint32_t e0, uint32_t n0) {
+                                          int dx0, int nk, int min_support, float m0, uint32_t e0, uint32_t n0,
+                                          const uint8_t *cnt8 = nullptr, int cw = 0) {
     constexpr int KL = kFK / 2;
     float acc[7], thr[7];
     int cnt[7];
@@ -140,12 +143,17 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
 #pragma unroll
     for (int j = 0; j < kFK; ++j) colm |= (xx + j >= 0 && xx + j < g.W) ? (1u << j) : 0u;
     // 1. Supports n'(delta) (R6, R9): slots holding a term.
-#pragma unroll 1
-    for (int oy = 0; oy < kFK; ++oy) {
-        const uint32_t rb = (xy + oy >= 0 && xy + oy < g.H) ? colm : 0u;
-        const uint32_t bits = mask_bits(g, crow + oy, ccol);
+    if (cnt8 && colm == 0xffu && xy >= 0 && xy + kFK <= g.H) {
 #pragma unroll
-        for (int k = 0; k < 7; ++k) cnt[k] += __popc((bits >> pat_j<PAT>(k)) & rb);
+        for (int k = 0; k < 7; ++k) cnt[k] = cnt8[crow * cw + ccol + pat_j<PAT>(k)];
+    } else {
+#pragma unroll 1
+        for (int oy = 0; oy < kFK; ++oy) {
+            const uint32_t rb = (xy + oy >= 0 && xy + oy < g.H) ? colm : 0u;
+            const uint32_t bits = mask_bits(g, crow + oy, ccol);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) cnt[k] += __popc((bits >> pat_j<PAT>(k)) & rb);
+        }
     }
     // 2. Settled deltas: out of the set, delta = 0, SENTINEL (n' < min_support never rejects, R11);
     //    thresholds of the rest.

@@ -28,6 +28,15 @@ __device__ __forceinline__ constexpr int pat_j(int k) {
     return PAT == 0 ? (k == 0 ? 0 : k == 1 ? 4 : k == 2 ? 6 : k == 3 ? 7 : k == 4 ? 8 : k == 5 ? 10 : 14) : k;
 }
 
+// Packed fp32x2 subtraction (sm_100a FADD2) of (a0, a1) - (b0, b1), per-lane IEEE round-to-nearest.
+__device__ __forceinline__ void sub2(float a0, float a1, float b0, float b1, float &d0, float &d1) {
+    unsigned long long x, y, r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b0), "f"(b1));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(r));
+}
+
 struct Regions {
     int cy0, cx0, CR, CC, cpitch, mwords;   // current region: global row/col of element 0, sizes
     int ry0, rx0, RR, RC, rpitch;           // reference region
@@ -181,10 +190,18 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
         for (int k = 0; k < 7; ++k) {
             const int j = pat_j<PAT>(k);
             const uint32_t vm = (bits >> j) & rb;              // slots holding a term (R9)
+            float dd[kFK];
+            if ((j & 1) == 0) {
+                // even offsets: differences of aligned register pairs in one FADD2 each
+#pragma unroll
+                for (int ox = 0; ox < kFK; ox += 2) sub2(r[ox], r[ox + 1], c[ox + j], c[ox + j + 1], dd[ox], dd[ox + 1]);
+            } else {
+#pragma unroll
+                for (int ox = 0; ox < kFK; ++ox) dd[ox] = __fsub_rn(r[ox], c[ox + j]);
+            }
 #pragma unroll
             for (int ox = 0; ox < kFK; ++ox) {
-                const float d = __fsub_rn(r[ox], c[ox + j]);
-                const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
+                const float t = SSD ? __fmul_rn(dd[ox], dd[ox]) : fabsf(dd[ox]);
                 if (vm & (1u << ox)) acc[k] = __fadd_rn(acc[k], t);   // row-major order, terms only
             }
             if (acc[k] >= thr[k]) settled |= 1u << k;

@@ -334,3 +334,22 @@ def test_deterministic_repeat():
     a, ea = gpu_me(inp, K=8, S=16, fuse=qs.make_checks())
     b, eb = gpu_me(inp, K=8, S=16, fuse=qs.make_checks())
     assert_field_equal(a, b) and ea == eb
+
+
+# ---------------------------------------------------------------------------
+# Quarter-sampling body: interior and border tiles (clip-free phase, npx entry, support-plane
+# phase 2), parity chunks with a partial last group (2S+1 = 15 for S = 7)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("S,ssd,f32", [(4, False, False), (7, False, False), (7, True, False), (9, False, True),
+                                       (16, False, False), (16, True, True)])
+def test_quad_interior_and_border_tiles(S, ssd, f32):
+    seq = synth.make_sequence(4 if f32 else 2, w=256, h=224)
+    inp = synth.pair_inputs(seq, 5, 2)
+    assert (inp["ref"].dtype == np.float32) == f32
+    g, _ = gpu_me(inp, K=8, S=S, ssd=ssd)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=8, S=S, ssd=ssd)
+    if f32:
+        ties = f32_me_compare(g, o, inp, 8, S, ssd=ssd)
+        assert len(ties) <= max(3, int(1e-3 * (o["status"] == oracle.CANDIDATE).sum())), ties
+    else:
+        assert_field_equal(g, o, what=f"quad S={S} ssd={ssd}")

@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--variants", action="store_true", help="also time the CC variants (RME, RMC, FRMC, NNC->FRMC)")
+    ap.add_argument("--sequential-pairs", dest="concurrent_pairs", action="store_false",
+                    help="run the three pairs of a step in order on one stream (default: one stream per pair)")
     return ap.parse_args()
 
 
@@ -182,16 +184,38 @@ def run_ours(args):
     acc_s, acc_c = qs.alloc_acc(band.rows, W, dev)
     evals = torch.zeros(1, dtype=torch.int64, device=dev)
 
+    main = torch.cuda.current_stream(dev)
+    pair_streams = [torch.cuda.Stream(dev) for _ in range(3)]
+
     def step(t):
         if world > 1:
             rowband.exchange_halo(dfr[t - 1]["ref"], band)
         acc_s.zero_()
         acc_c.zero_()
+        if not args.concurrent_pairs:
+            for d in (1, 2, 3):
+                fr, past = dfr[t], dfr[t - d]
+                qs.qs_me_search(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1], fuse=checks,
+                                eval_count=evals, ws=wss[d - 1])
+                qs.qs_project(fields[d - 1], past["cur"], past["mask"], roi, acc_s, acc_c)
+            return
+        # The three (frame, reference) pairs are independent until PR: ME + checks of each pair on its
+        # own stream (fills the tail waves of one pair with the next), PR serialised on the main stream.
+        start = torch.cuda.Event()
+        start.record(main)
+        done = []
         for d in (1, 2, 3):
+            ps = pair_streams[d - 1]
+            ps.wait_event(start)
             fr, past = dfr[t], dfr[t - d]
             qs.qs_me_search(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1], fuse=checks,
-                            eval_count=evals, ws=wss[d - 1])
-            qs.qs_project(fields[d - 1], past["cur"], past["mask"], roi, acc_s, acc_c)
+                            eval_count=evals, ws=wss[d - 1], stream=ps)
+            ev = torch.cuda.Event()
+            ev.record(ps)
+            done.append(ev)
+        for d in (1, 2, 3):
+            main.wait_event(done[d - 1])
+            qs.qs_project(fields[d - 1], dfr[t - d]["cur"], dfr[t - d]["mask"], roi, acc_s, acc_c)
 
     order = step_order(args.frames, args.warmup + args.steps)
     for t in order[:args.warmup]:
@@ -200,7 +224,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     qs.qs_profile_reset()
-    qs.qs_profile_enable(True)
+    # Per-launch kernel timing (qs_profile: CUDA events on each launch's stream) is taken in the timed
+    # region when the pairs run in order; with concurrent pairs the launches overlap, so the
+    # per-kernel numbers come from a sequential pass over the same steps right after it.
+    qs.qs_profile_enable(not args.concurrent_pairs)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         if world > 1:
@@ -215,8 +242,19 @@ def run_ours(args):
             dist.barrier()
     qs.qs_profile_enable(False)
     ms = t0.elapsed_time(t1)
+    launches = sum(n for _, n in (qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS))
+    if args.concurrent_pairs:
+        args.concurrent_pairs = False
+        qs.qs_profile_reset()
+        qs.qs_profile_enable(True)
+        for t in order[args.warmup:]:
+            step(t)
+        torch.cuda.synchronize()
+        qs.qs_profile_enable(False)
+        args.concurrent_pairs = True
     prof = {k: qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS}
-    launches = sum(n for _, n in prof.values())
+    if args.concurrent_pairs:   # the same steps launch the same kernels in either order
+        launches = sum(n for _, n in prof.values())
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -258,6 +296,8 @@ def run_ours(args):
                "config": {"workload": cfg.name, "frame": f"{W}x{H}", "K": K, "S": S, "refs": 3,
                           "mask": "dynamic" if cfg.dynamic else "fixed", "check": args.check,
                           "parallelism": f"rowband{world}" if world > 1 else "single",
+                          "pairs": "3 streams (one per reference d; PR in order)" if args.concurrent_pairs else "in order",
+                          "kernel_timing": "sequential pass over the same steps" if args.concurrent_pairs else "timed region",
                           "l2": "24 resident frames (~345 MB > 126 MB L2); consecutive steps use disjoint frames"},
                "roofline": roofline, "kernel_ms_per_step": kernel_ms, "gpu_launches": launches,
                "clocks": clk.summary(), "e2e": e2e, "impl": "ours"}
@@ -297,6 +337,7 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
     out_c = torch.empty((band.rows, W), dtype=torch.uint8).pin_memory()
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
+    pair_streams = [torch.cuda.Stream(dev) for _ in range(3)]
     counts = {"h2d": 0, "d2h": 0}
 
     def issue_copies(i, ts, used_by):
@@ -326,10 +367,26 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
                 ready_next = issue_copies(i + 1, ts, done[(i + 1) % 2])
             acc_s.zero_()
             acc_c.zero_()
-            for d in (1, 2, 3):
-                qs.qs_me_search(slots[0]["cur"], slots[0]["mask"], slots[d]["ref"], roi, prm, fields[d - 1],
-                                fuse=checks, ws=wss[d - 1])
-                qs.qs_project(fields[d - 1], slots[d]["cur"], slots[d]["mask"], roi, acc_s, acc_c)
+            if args.concurrent_pairs:
+                start = torch.cuda.Event()
+                start.record(comp)
+                pev = []
+                for d in (1, 2, 3):
+                    ps = pair_streams[d - 1]
+                    ps.wait_event(start)
+                    qs.qs_me_search(slots[0]["cur"], slots[0]["mask"], slots[d]["ref"], roi, prm, fields[d - 1],
+                                    fuse=checks, ws=wss[d - 1], stream=ps)
+                    e = torch.cuda.Event()
+                    e.record(ps)
+                    pev.append(e)
+                for d in (1, 2, 3):
+                    comp.wait_event(pev[d - 1])
+                    qs.qs_project(fields[d - 1], slots[d]["cur"], slots[d]["mask"], roi, acc_s, acc_c)
+            else:
+                for d in (1, 2, 3):
+                    qs.qs_me_search(slots[0]["cur"], slots[0]["mask"], slots[d]["ref"], roi, prm, fields[d - 1],
+                                    fuse=checks, ws=wss[d - 1])
+                    qs.qs_project(fields[d - 1], slots[d]["cur"], slots[d]["mask"], roi, acc_s, acc_c)
             out_s.copy_(acc_s, non_blocking=True)
             out_c.copy_(acc_c, non_blocking=True)
             counts["d2h"] += out_s.numel() * 4 + out_c.numel()

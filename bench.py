@@ -417,30 +417,37 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
 
 
 def run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32):
-    """GPU analogue of Table 3's CC column: per-frame check time for each variant (3 references)."""
+    """GPU analogue of Table 3's CC column: per-frame check time for each variant (3 references),
+    after an untimed warm-up pass of the variant's kernels."""
     res = {}
     t = 7
+
+    def check(name, d, fr, past):
+        f, ws = fields[d - 1], wss[d - 1]
+        if name == "nnc_frmc":
+            qs.qs_nnc(f, roi)
+            qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, f)
+        elif name == "frmc":
+            qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, f)
+        elif name == "rme":
+            qs.qs_reverse_check(qs.QS_RME, fr["cur"], fr["mask"], past["ref"], roi, prm, f, ws=ws)
+        else:
+            qs.qs_reverse_check(qs.QS_RMC, fr["cur"], fr["mask"], past["ref"], roi, prm, f)
+
     for name in ("nnc_frmc", "frmc", "rme", "rmc"):
         tot = 0.0
-        for d in (1, 2, 3):
-            fr, past = dfr[t], dfr[t - d]
-            qs.qs_me_search(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1], ws=wss[d - 1])
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            if name == "nnc_frmc":
-                qs.qs_nnc(fields[d - 1], roi)
-                qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1])
-            elif name == "frmc":
-                qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1])
-            elif name == "rme":
-                qs.qs_reverse_check(qs.QS_RME, fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1],
-                                    ws=wss[d - 1])
-            else:
-                qs.qs_reverse_check(qs.QS_RMC, fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1])
-            b.record()
-            torch.cuda.synchronize()
-            tot += a.elapsed_time(b)
+        for rep in range(2):                 # rep 0: warm-up
+            for d in (1, 2, 3):
+                fr, past = dfr[t], dfr[t - d]
+                qs.qs_me_search(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1], ws=wss[d - 1])
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                check(name, d, fr, past)
+                b.record()
+                torch.cuda.synchronize()
+                if rep:
+                    tot += a.elapsed_time(b)
         res[name] = round(tot, 3)
     return res
 

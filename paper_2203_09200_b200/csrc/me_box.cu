@@ -27,6 +27,7 @@
 // the order key is monotone in the mean and equal means give equal keys.
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 
 #include "qs_internal.cuh"
 
@@ -307,15 +308,19 @@ constexpr int kQHC = kQBX;              // 32 H columns (D already carries the k
 constexpr int kQHP = kQHC + 1;          // H plane row pitch in packed pairs (66 words = 2 mod 4: conflict-free STS.64)
 constexpr int kQRun = 8;                // H columns per producer warp (4 x 8 = 32)
 constexpr int kQG = kQRun + 4;          // blocks read per producer lane (12: k = j-2 .. j+1, +1 for D)
+// Interior tiles: two producer warp pairs (even / odd candidates), 16 H columns per lane.
+constexpr int kQRunI = 16;
+constexpr int kQGI = kQRunI + 4;        // 20 blocks read per interior producer lane
+constexpr int kQBarI = 64 + 128;        // threads on an interior FULL / EMPTY barrier: one producer pair + consumers
 constexpr int kQSeg = kQBY / 2;         // 14 output block rows per consumer lane (2 row halves x C/D planes)
 constexpr int kQWinRows = 2 * kQHR;     // 64 pixel rows of blocks per tile (+ alpha range)
 constexpr int kQWinCols = 2 * (4 * kQRun + 4);  // 72 pixel columns (blocks -2 .. 33)
 
 // Named barriers with immediate ids (1..4), so ptxas reserves only the ones used.
-template <int ID>
-__device__ __forceinline__ void nb_sync_i() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(kNT) : "memory"); }
-template <int ID>
-__device__ __forceinline__ void nb_arrive_i() { asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(kNT) : "memory"); }
+template <int ID, int CNT = kNT>
+__device__ __forceinline__ void nb_sync_i() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(CNT) : "memory"); }
+template <int ID, int CNT = kNT>
+__device__ __forceinline__ void nb_arrive_i() { asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(CNT) : "memory"); }
 __device__ __forceinline__ void nb_sync(int id, int) {
     switch (id) {
         case 1: nb_sync_i<1>(); break;
@@ -494,6 +499,124 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     const int e1 = nA + ((BORDER && nA > 0) ? 1 : 0);   // entries of phase 1 (+ the npx entry)
     const int n_ent = e1 + nB;
     if (n_ent <= 0) return;                              // uniform
+
+    if constexpr (!BORDER) {
+        // ------------------- interior: warp-specialised registers -------------------
+        // Producers: two warp pairs; pair p = (warp >> 1) reduces the candidates k = p, p + 2, ...
+        // into ring stage p, warp half = warp & 1 of a pair takes H columns 16 half .. +15 (20 blocks
+        // gathered per lane: 1.25x the columns instead of 1.5x).  setmaxnreg: producers 152, consumers
+        // 104 registers (the 20 blocks' statics).  FULL[p] / EMPTY[p] = named barriers 1 + p / 5 + p
+        // over the 64 threads of pair p and the 128 consumers.
+        if (warp < 4) {
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
+            const int hr = lane, bi = hr - 2;
+            const int pair = warp >> 1, half = warp & 1;
+            float cv[kQGI], wx[kQGI];
+            f2_t wy2[kQGI];
+            int ad[kQGI];
+#pragma unroll
+            for (int kk = 0; kk < kQGI; ++kk) {
+                const int bk = kQRunI * half - 2 + kk;
+                const int y = py0 + 2 * bi, x = px0 + 2 * bk;
+                const int64_t r = (int64_t)(y - a.buf_y0);
+                const uint8_t *m0 = a.mask.p + r * a.mask.pitch + x;
+                const int q = m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
+                const int dy = q >> 1, dx = q & 1;
+                cv[kk] = (float)a.cur.p[(r + dy) * a.cur.pitch + x + dx];
+                wy2[kk] = f2pack((float)(1 - dy), (float)dy);
+                wx[kk] = (float)dx;
+                ad[kk] = 4 * (dy * bplane + (bi + 2) * bpitch + (2 * bk + dx + 4 + a.S));
+            }
+            const unsigned hbase = (unsigned)__cvta_generic_to_shared(Hp + hr * kQHP + kQRunI * half);
+            auto run = [&](auto Pc) {   // Pc = std::integral_constant pair (compile-time barrier ids)
+                constexpr int P = decltype(Pc)::value;
+                const unsigned hs = hbase + (unsigned)P * kStageBytes;
+                float rv[kQGI];
+                auto gather = [&](int ci) {
+                    const int pk = clist[ci];
+                    const char *bwc = reinterpret_cast<const char *>(
+                        Bw + (((int)(int8_t)(pk & 0xff) - alo) >> 1) * bpitch + (int)(int8_t)((pk >> 8) & 0xff));
+#pragma unroll
+                    for (int kk = 0; kk < kQGI; ++kk) rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
+                };
+                for (int k = P; k < nA; k += 2) {
+                    gather(k);
+                    if (k >= 2) nb_sync_i<5 + P, kQBarI>();           // EMPTY[P]: candidate k-2 was read
+                    f2_t u[kQGI], m[kQGI - 1], pu[kQGI - 1], pm[kQGI - 2], gp = 0ull;
+#pragma unroll
+                    for (int kk = 0; kk < kQGI; ++kk) {
+                        const float d = __fsub_rn(cv[kk], rv[kk]);
+                        const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
+                        u[kk] = f2mul(f2pack(t, t), wy2[kk]);
+                        const f2_t g1 = f2mul(u[kk], f2pack(wx[kk], wx[kk]));
+                        if (kk > 0) m[kk - 1] = f2add(gp, f2sub(u[kk], g1));
+                        gp = g1;
+                        if (kk >= 1) pu[kk - 1] = f2add(u[kk - 1], u[kk]);
+                        if (kk >= 2) pm[kk - 2] = f2add(m[kk - 2], m[kk - 1]);
+                        if (kk >= 3 && kk - 3 < kQRunI) st_shared_f2(hs + 8 * (kk - 3), f2add(pu[kk - 3], pu[kk - 1]));
+                        if (kk >= 4 && kk - 4 < kQRunI)
+                            st_shared_f2(hs + 8 * (kPlane + kk - 4), f2add(pm[kk - 4], pm[kk - 2]));
+                    }
+                    nb_arrive_i<1 + P, kQBarI>();                       // FULL[P]
+                }
+                if (P < nA) nb_sync_i<5 + P, kQBarI>();                // drain: the last candidate was read
+            };
+            if (pair == 0) run(std::integral_constant<int, 0>{});
+            else run(std::integral_constant<int, 1>{});
+        } else {
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
+            const int j = lane;
+            const int cw = warp - 4, pl = cw & 1, i0 = kQSeg * (cw >> 1);
+            float be[kQSeg][2];
+            int br[kQSeg][2];
+#pragma unroll
+            for (int r = 0; r < kQSeg; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) { be[r][c] = INFINITY; br[r][c] = -1; }
+            const unsigned cbase = (unsigned)__cvta_generic_to_shared(Hp + pl * kPlane + i0 * kQHP + j);
+            auto consume = [&](int k, auto Pc) {
+                constexpr int P = decltype(Pc)::value;
+                const int rank = clist[k] >> 16;
+                nb_sync_i<1 + P, kQBarI>();                             // FULL[P]
+                const unsigned cs = cbase + (unsigned)P * kStageBytes;
+                f2_t x[kQSeg + 4];
+#pragma unroll
+                for (int t = 0; t < kQSeg + 4; ++t) x[t] = ld_shared_f2(cs + 8 * t * kQHP);
+                nb_arrive_i<5 + P, kQBarI>();                           // EMPTY[P]
+                f2_t pp0 = f2add(x[0], x[1]), pp1 = f2add(x[1], x[2]), pp2 = f2add(x[2], x[3]);
+                f2_t pp3 = f2add(x[3], x[4]);
+                f2_t vcur = f2add(pp0, pp2);
+#pragma unroll
+                for (int r = 0; r < kQSeg; ++r) {
+                    const f2_t vnext = f2add(pp1, pp3);
+                    const float ev[2] = {__fadd_rn(f2lo(vcur), f2hi(vcur)), __fadd_rn(f2hi(vcur), f2lo(vnext))};
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+                        if (ev[c] < be[r][c]) { be[r][c] = ev[c]; br[r][c] = rank; }
+                    vcur = vnext;
+                    pp0 = pp1;
+                    pp1 = pp2;
+                    pp2 = pp3;
+                    if (r + 5 < kQSeg + 4) pp3 = f2add(x[r + 4], x[r + 5]);
+                }
+            };
+            for (int k = 0; k < nA; k += 2) {
+                consume(k, std::integral_constant<int, 0>{});
+                if (k + 1 < nA) consume(k + 1, std::integral_constant<int, 1>{});
+            }
+#pragma unroll
+            for (int r = 0; r < kQSeg; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
+                    if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
+                    const unsigned long long key =
+                        ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
+                    atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+                }
+        }
+        return;
+    }
 
     if (warp < 4) {
         // ------------------------------ producer ------------------------------

@@ -70,17 +70,31 @@ def exchange_halo(plane: torch.Tensor, band: Band, group=None) -> None:
     r, h, H = band.rank, band.h, band.H
     own0 = band.y0 - band.b0          # buffer row of the first owned row
     own1 = band.y1 - band.b0          # buffer row one past the last owned row
-    ops = []
+    ops, landing = [], []
+
+    def recv(rows):
+        # pitched planes (row pitch > width) give non-contiguous row slices: receive into a
+        # contiguous buffer and copy it in after the wait
+        dst = rows if rows.is_contiguous() else torch.empty(rows.shape, dtype=rows.dtype, device=rows.device)
+        if dst is not rows:
+            landing.append((rows, dst))
+        return dst
+
+    def send(rows):
+        return rows if rows.is_contiguous() else rows.contiguous()
+
     if r > 0:
         n_recv = min(h, band.y0)                   # my top halo
         n_send = min(h, H - band.y0)               # the upper neighbour's bottom halo = my first rows
         n_send = min(n_send, own1 - own0)
-        ops.append(dist.P2POp(dist.irecv, plane[own0 - n_recv:own0], r - 1, group))
-        ops.append(dist.P2POp(dist.isend, plane[own0:own0 + n_send], r - 1, group))
+        ops.append(dist.P2POp(dist.irecv, recv(plane[own0 - n_recv:own0]), r - 1, group))
+        ops.append(dist.P2POp(dist.isend, send(plane[own0:own0 + n_send]), r - 1, group))
     if r < band.world - 1:
         n_recv = min(h, H - band.y1)               # my bottom halo
         n_send = min(h, band.y1, own1 - own0)      # the lower neighbour's top halo = my last rows
-        ops.append(dist.P2POp(dist.isend, plane[own1 - n_send:own1], r + 1, group))
-        ops.append(dist.P2POp(dist.irecv, plane[own1:own1 + n_recv], r + 1, group))
+        ops.append(dist.P2POp(dist.isend, send(plane[own1 - n_send:own1]), r + 1, group))
+        ops.append(dist.P2POp(dist.irecv, recv(plane[own1:own1 + n_recv]), r + 1, group))
     for q in dist.batch_isend_irecv(ops):
         q.wait()
+    for rows, buf in landing:
+        rows.copy_(buf)

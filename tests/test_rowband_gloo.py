@@ -38,14 +38,15 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, H, W, h, q):
+def _worker(rank, world, port, H, W, h, q, pitch=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         band = rowband.band_of(rank, world, H, h)
         glob = torch.arange(H * W, dtype=torch.float32).reshape(H, W)
-        plane = torch.full((band.rows, W), float("nan"))
+        # a pitched plane (row pitch > width, as qs.pitched gives): non-contiguous row slices
+        plane = torch.full((band.rows, pitch or W), float("nan"))[:, :W]
         plane[band.y0 - band.b0:band.y1 - band.b0] = glob[band.y0:band.y1]   # only owned rows exist
         rowband.exchange_halo(plane, band)
         ok = torch.equal(plane, glob[band.b0:band.b1])
@@ -54,14 +55,14 @@ def _worker(rank, world, port, H, W, h, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_halo_exchange_gloo(world):
+@pytest.mark.parametrize("world,pitch", [(2, None), (3, None), (2, 20)])
+def test_halo_exchange_gloo(world, pitch):
     H, W = 120, 16
     h = rowband.halo_rows(8, 8)     # 14 rows
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, h, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, H, W, h, q, pitch)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in range(world))

@@ -353,3 +353,18 @@ def test_quad_interior_and_border_tiles(S, ssd, f32):
         assert len(ties) <= max(3, int(1e-3 * (o["status"] == oracle.CANDIDATE).sum())), ties
     else:
         assert_field_equal(g, o, what=f"quad S={S} ssd={ssd}")
+
+
+# ---------------------------------------------------------------------------
+# Check variants: FRMC with the {0, +-(2^k - 1)} offsets extended to a large S
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("f32", [False, True])
+def test_frmc_extended_offsets(f32):
+    seq = synth.make_sequence(4 if f32 else 3, w=160, h=128)
+    inp = synth.pair_inputs(seq, 6, 2)
+    S = 16
+    offs = (-15, -7, -3, -1, 0, 1, 3, 7, 15)
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=8, S=S)
+    st, ev = gpu_check("frmc", inp, o, K=8, S=S, offsets=offs)
+    ost, oev = oracle.frmc(inp["cur"], inp["cur_mask"], inp["ref"], o, offsets=offs, K=8, S=S)
+    assert np.array_equal(st, ost) and ev == oev

@@ -175,6 +175,38 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
         else thr[k] = n0 ? (float)(((unsigned long long)e0 * (unsigned)cnt[k] + n0 - 1) / n0) : INFINITY;   // ceil(e0 n'/n0)
     }
     // 3. Reverse costs, row-major, until every delta is settled.
+    if (colm == 0xffu && xy >= 0 && xy + kFK <= g.H) {
+        // Reference window in the frame: the term predicate of slot (delta_x = k, ox) is bit
+        // j_k + ox of the row's current-mask segment, so the 22 segment bits serve all 56 slots.
+        // Walking the bit positions in ascending order visits each delta's slots in ascending ox:
+        // the accumulation order is the definition's row-major order.
+#pragma unroll 1
+        for (int oy = 0; oy < kFK && settled != 0x7fu; ++oy) {
+            const float *cp = g.Cs + (crow + oy) * g.cpitch + ccol;
+            const float *rp = g.Rs + (rrow + oy) * g.rpitch + rcol;
+            float c[kFSeg], r[kFK];
+#pragma unroll
+            for (int j = 0; j < kFSeg; ++j) c[j] = cp[j];
+#pragma unroll
+            for (int j = 0; j < kFK; ++j) r[j] = rp[j];
+            const uint32_t bits = mask_bits(g, crow + oy, ccol);
+#pragma unroll
+            for (int b = 0; b < kFSeg; ++b) {
+                const bool term = (bits >> b) & 1u;
+#pragma unroll
+                for (int k = 0; k < 7; ++k) {
+                    const int ox = b - pat_j<PAT>(k);
+                    if (ox < 0 || ox >= kFK) continue;
+                    const float d = __fsub_rn(r[ox], c[b]);
+                    const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
+                    if (term) acc[k] = __fadd_rn(acc[k], t);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 7; ++k)
+                if (acc[k] >= thr[k]) settled |= 1u << k;
+        }
+    } else {
 #pragma unroll 1
     for (int oy = 0; oy < kFK && settled != 0x7fu; ++oy) {
         const float *cp = g.Cs + (crow + oy) * g.cpitch + ccol;
@@ -206,6 +238,7 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
             }
             if (acc[k] >= thr[k]) settled |= 1u << k;
         }
+    }
     }
     if (settled == 0x7fu) return false;
     bool reject = false;

@@ -15,6 +15,8 @@ SURVEY.md §8(e)); each step first exchanges the newest reference's halo rows wi
 neighbouring ranks (NCCL P2P), then runs the path on its band.  Timed on the device with CUDA
 events, max over ranks.  Inputs: 24 resident frames (> L2); consecutive steps use disjoint
 frames (stride 4), so no step finds its inputs in L2 from the previous one.
+--sequences (e.g. --config 5 --frames 12): rank r runs sequence r on the whole frame, no collective
+in the step (SURVEY.md §8(e) mode (i)); value = all ranks' pixels / max rank time, weak scaling.
 """
 from __future__ import annotations
 
@@ -50,6 +52,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--variants", action="store_true", help="also time the CC variants (RME, RMC, FRMC, NNC->FRMC)")
+    ap.add_argument("--sequences", action="store_true",
+                    help="independent sequences: rank r runs sequence s = r of the config on the whole frame "
+                         "(SURVEY.md 8(e) mode (i), config 5's batch; weak scaling, no collective in the step)")
     ap.add_argument("--sequential-pairs", dest="concurrent_pairs", action="store_false",
                     help="run the three pairs of a step in order on one stream (default: one stream per pair)")
     return ap.parse_args()
@@ -115,9 +120,9 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # Inputs
 # ---------------------------------------------------------------------------
-def make_frames(cfg: int, n_frames: int):
+def make_frames(cfg: int, n_frames: int, s: int = 0):
     import synth
-    seq = synth.make_sequence(cfg)
+    seq = synth.make_sequence(cfg, s)
     frames = []
     for t in range(n_frames):
         m = seq.mask(t)
@@ -157,8 +162,13 @@ def run_ours(args):
     cfg = synth.CONFIGS[args.config]
     W, H, K, S = cfg.w, cfg.h, cfg.K, cfg.S
     f32 = cfg.ref_f32
-    band = rowband.band_of(rank, world, H, rowband.halo_rows(S, K))
-    seq, frames = make_frames(args.config, args.frames)
+    if args.sequences:   # one whole sequence per rank
+        band = rowband.band_of(0, 1, H, rowband.halo_rows(S, K))
+        seq, frames = make_frames(args.config, args.frames, s=rank)
+    else:
+        band = rowband.band_of(rank, world, H, rowband.halo_rows(S, K))
+        seq, frames = make_frames(args.config, args.frames)
+    banded = world > 1 and not args.sequences
 
     # Device-resident band buffers (row i = global row band.b0 + i).
     def dplane(a):
@@ -167,11 +177,11 @@ def run_ours(args):
     dfr = []
     for fr in frames:
         ref = dplane(fr["ref"])
-        if world > 1:   # the reconstruction exists only for owned rows until the halo exchange
+        if banded:      # the reconstruction exists only for owned rows until the halo exchange
             ref[:band.y0 - band.b0] = float("nan") if f32 else 0
             ref[band.y1 - band.b0:] = float("nan") if f32 else 0
         dfr.append(dict(cur=dplane(fr["cur"]), mask=dplane(fr["mask"]), ref=ref))
-    if world > 1:       # each frame's reference halo, as it would have arrived when it was newest
+    if banded:          # each frame's reference halo, as it would have arrived when it was newest
         for d in dfr:
             rowband.exchange_halo(d["ref"], band)
     torch.cuda.synchronize()
@@ -188,7 +198,7 @@ def run_ours(args):
     pair_streams = [torch.cuda.Stream(dev) for _ in range(3)]
 
     def step(t):
-        if world > 1:
+        if banded:
             rowband.exchange_halo(dfr[t - 1]["ref"], band)
         acc_s.zero_()
         acc_c.zero_()
@@ -259,7 +269,8 @@ def run_ours(args):
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    value = args.steps * W * H / (ms / 1e3) / 1e6
+    n_seq = world if args.sequences else 1
+    value = n_seq * args.steps * W * H / (ms / 1e3) / 1e6
 
     # Roofline of the dominant kernel (me_box).
     me_ms, me_n = prof["me_box"]
@@ -291,14 +302,16 @@ def run_ours(args):
     if rank == 0:
         out = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "higher_is_better": True, "scaling": "weak" if args.sequences else "strong", "vs_baseline": None,
                "dtype": "f32" if f32 else "u8->f32(exact)", "data": "synthetic",
                "config": {"workload": cfg.name, "frame": f"{W}x{H}", "K": K, "S": S, "refs": 3,
                           "mask": "dynamic" if cfg.dynamic else "fixed", "check": args.check,
-                          "parallelism": f"rowband{world}" if world > 1 else "single",
+                          "parallelism": (f"sequences{world}" if args.sequences else f"rowband{world}") if world > 1
+                          else "single",
                           "pairs": "3 streams (one per reference d; PR in order)" if args.concurrent_pairs else "in order",
                           "kernel_timing": "sequential pass over the same steps" if args.concurrent_pairs else "timed region",
-                          "l2": "24 resident frames (~345 MB > 126 MB L2); consecutive steps use disjoint frames"},
+                          "l2": f"{args.frames} resident frames (~{args.frames * W * H * (6 if f32 else 3) / 1e6:.0f} MB vs "
+                                f"126 MB L2); consecutive steps use disjoint frames"},
                "roofline": roofline, "kernel_ms_per_step": kernel_ms, "gpu_launches": launches,
                "clocks": clk.summary(), "e2e": e2e, "impl": "ours"}
         if args.variants:
@@ -411,7 +424,8 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    return {"value": round(args.steps * W * H / (ms / 1e3) / 1e6, 3), "unit": "Mpixel/s",
+    n_seq = world if args.sequences else 1
+    return {"value": round(n_seq * args.steps * W * H / (ms / 1e3) / 1e6, 3), "unit": "Mpixel/s",
             "h2d_bytes_per_step": counts["h2d"] // args.steps, "d2h_bytes_per_step": counts["d2h"] // args.steps,
             "ms_per_step": round(ms / args.steps, 4), "overlap": "H2D of step i+1 on a copy stream during step i"}
 

@@ -223,6 +223,10 @@ __global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g)
     float *ent_m0 = reinterpret_cast<float *>(ent + kFT * kFT);
     uint32_t *ent_e0 = reinterpret_cast<uint32_t *>(ent_m0 + kFT * kFT);
     uint8_t *rej = reinterpret_cast<uint8_t *>(ent_e0 + kFT * kFT);
+    // measured pixels of the current 8x8 window at each region position (supports of entries whose
+    // reference window lies in the frame, tile::frmc_item)
+    const int cw = kFT + 2 * g.maxd;
+    uint8_t *cnt8 = rej + kFT * kFT;
     __shared__ int n_ent;
     const int tid = threadIdx.x;
     if (tid == 0) n_ent = 0;
@@ -249,6 +253,13 @@ __global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g)
             }
         }
     }
+    for (int i = tid; i < cw * cw; i += blockDim.x) {
+        const int r = i / cw, c = i - r * cw;
+        int n = 0;
+#pragma unroll
+        for (int oy = 0; oy < kFK; ++oy) n += __popc(tile::mask_bits(R, r + oy, c) & 0xffu);
+        cnt8[i] = (uint8_t)n;
+    }
     __syncthreads();
     const int ne = n_ent;
     const int per_entry = g.n_dy * g.n_groups;
@@ -267,7 +278,7 @@ __global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g)
         const int nk = PAT == 0 ? 7 : (grp == g.n_groups - 1 ? g.n_last : 7);
         const uint32_t n0 = F32 ? ent_e0[e] : (uint32_t)__float_as_int(ent_m0[e]);
         if (tile::frmc_item<PAT, SSD, F32>(R, ty0, tx0, ly, lx, va, vb, dy, dx0, nk, a.min_support, ent_m0[e],
-                                           ent_e0[e], n0))
+                                           ent_e0[e], n0, cnt8, cw))
             rej[e] = 1;
     }
     __syncthreads();
@@ -282,7 +293,8 @@ __global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g)
 template <int PAT, bool SSD, bool F32>
 cudaError_t launch_tile_t(const TileGridArgs &g, cudaStream_t s) {
     const size_t smem = tile::RegionSizes(g.maxd, g.S).bytes() +
-                        (sizeof(int) + sizeof(float) + sizeof(uint32_t) + 1) * kFT * kFT + 16;
+                        (sizeof(int) + sizeof(float) + sizeof(uint32_t) + 1) * kFT * kFT +
+                        (size_t)(kFT + 2 * g.maxd) * (kFT + 2 * g.maxd) + 16;
     auto fn = revgrid_tile_kernel<PAT, SSD, F32>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -448,8 +448,10 @@ def run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32):
         else:
             qs.qs_reverse_check(qs.QS_RMC, fr["cur"], fr["mask"], past["ref"], roi, prm, f)
 
+    rates = {}
     for name in ("nnc_frmc", "frmc", "rme", "rmc"):
         tot = 0.0
+        acc = cand = 0
         for rep in range(2):                 # rep 0: warm-up
             for d in (1, 2, 3):
                 fr, past = dfr[t], dfr[t - d]
@@ -462,7 +464,12 @@ def run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32):
                 torch.cuda.synchronize()
                 if rep:
                     tot += a.elapsed_time(b)
+                    st = fields[d - 1].status
+                    acc += int((st == qs.QS_ACCEPTED).sum().item())
+                    cand += int((st >= qs.QS_CANDIDATE).sum().item())
         res[name] = round(tot, 3)
+        rates[name] = round(acc / max(cand, 1), 4)
+    res["accept_rate"] = rates       # ACCEPTED / (entries with a vector), 3 references
     return res
 
 

@@ -82,35 +82,41 @@ __device__ __forceinline__ Regions layout(float *sm, int ty0, int tx0, int maxd,
 }
 
 // Stage both regions (NaN outside the frame / the buffer window / unmeasured) and the
-// current mask bits.  Ends with __syncthreads().
+// current mask bits.  One warp per region row, 32 columns per step: no index division, and the
+// mask word of each 32 columns is the warp's ballot.  Ends with __syncthreads().
 template <bool F32>
 __device__ __forceinline__ void stage(const Regions &g, const Plane &cur, const Plane &mask, const Plane &ref, int W,
                                       int H, int buf_y0, int buf_rows) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int i = tid; i < g.CR * g.mwords; i += nt) g.Mb[i] = 0u;
-    __syncthreads();
-    for (int i = tid; i < g.CR * g.cpitch; i += nt) {
-        const int r = i / g.cpitch, c = i - r * g.cpitch;
-        const int gy = g.cy0 + r, gx = g.cx0 + c;
-        float v = __int_as_float(0x7fc00000);
-        if (c < g.CC && gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= buf_y0 && gy < buf_y0 + buf_rows) {
-            const int64_t rr = gy - buf_y0;
-            if (mask.p[rr * mask.pitch + gx]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const float nan = __int_as_float(0x7fc00000);
+    for (int r = warp; r < g.CR; r += nw) {
+        const int gy = g.cy0 + r;
+        const bool row_ok = gy >= 0 && gy < H && gy >= buf_y0 && gy < buf_y0 + buf_rows;
+        const int64_t rr = gy - buf_y0;
+        for (int w = 0; w < g.mwords; ++w) {
+            const int c = 32 * w + lane, gx = g.cx0 + c;
+            bool meas = false;
+            float v = nan;
+            if (row_ok && c < g.CC && gx >= 0 && gx < W && mask.p[rr * mask.pitch + gx]) {
+                meas = true;
                 v = (float)cur.p[rr * cur.pitch + gx];
-                atomicOr(&g.Mb[r * g.mwords + (c >> 5)], 1u << (c & 31));
             }
+            if (c < g.cpitch) g.Cs[r * g.cpitch + c] = v;
+            const unsigned word = __ballot_sync(0xffffffffu, meas);
+            if (lane == 0) g.Mb[r * g.mwords + w] = word;
         }
-        g.Cs[i] = v;
     }
-    for (int i = tid; i < g.RR * g.rpitch; i += nt) {
-        const int r = i / g.rpitch, c = i - r * g.rpitch;
-        const int gy = g.ry0 + r, gx = g.rx0 + c;
-        float v = __int_as_float(0x7fc00000);
-        if (c < g.RC && gy >= 0 && gy < H && gx >= 0 && gx < W && gy >= buf_y0 && gy < buf_y0 + buf_rows) {
-            const int64_t rr = gy - buf_y0;
-            v = F32 ? reinterpret_cast<const float *>(ref.p + rr * ref.pitch)[gx] : (float)ref.p[rr * ref.pitch + gx];
+    for (int r = warp; r < g.RR; r += nw) {
+        const int gy = g.ry0 + r;
+        const bool row_ok = gy >= 0 && gy < H && gy >= buf_y0 && gy < buf_y0 + buf_rows;
+        const int64_t rr = gy - buf_y0;
+        for (int c = lane; c < g.rpitch; c += 32) {
+            const int gx = g.rx0 + c;
+            float v = nan;
+            if (row_ok && c < g.RC && gx >= 0 && gx < W)
+                v = F32 ? reinterpret_cast<const float *>(ref.p + rr * ref.pitch)[gx] : (float)ref.p[rr * ref.pitch + gx];
+            g.Rs[r * g.rpitch + c] = v;
         }
-        g.Rs[i] = v;
     }
     __syncthreads();
 }

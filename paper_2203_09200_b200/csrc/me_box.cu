@@ -630,10 +630,8 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         for (int kk = 0; kk < kQG; ++kk) {
             const int bk = kQRun * warp - 2 + kk;
             const int y = py0 + 2 * bi, x = px0 + 2 * bk;
-            bool inside = true;
-            if constexpr (BORDER)
-                inside = y >= 0 && y + 1 < a.H && x >= 0 && x + 1 < a.W && y >= a.buf_y0 &&
-                         y + 1 < a.buf_y0 + a.buf_rows;
+            const bool inside = y >= 0 && y + 1 < a.H && x >= 0 && x + 1 < a.W && y >= a.buf_y0 &&
+                                y + 1 < a.buf_y0 + a.buf_rows;
             int dy = 0, dx = 0;
             float c = 0.f;
             if (inside) {
@@ -692,7 +690,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             for (int kk = 0; kk < kQG; ++kk) {
                 const float d = mode == 1 ? 1.f : __fsub_rn(cv[kk], cur[kk]);
                 const float t0 = SSD ? __fmul_rn(d, d) : fabsf(d);
-                const float t = BORDER ? fmaxf(t0, 0.f) : t0;        // NaN (outside the frame) -> 0
+                const float t = fmaxf(t0, 0.f);                       // NaN (outside the frame) -> 0
                 roll(R, kk, t, hs, 0);
                 if (Q2 && mode == 2) roll(N, kk, (t0 == t0) ? 1.f : 0.f, hs, 2);   // term indicator
             }
@@ -718,13 +716,11 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         };
         static_assert(kQStages == 2, "stage ids are compile-time constants of the unrolled loops");
         run(0, nA, 0, 0);
-        if constexpr (BORDER) {
-            if (nA > 0) {
-                if (nA & 1) produce(nA, 1, ra, rb, -1, 1);
-                else produce(nA, 0, ra, rb, -1, 1);
-            }
-            if constexpr (Q2) run(nA, nB, e1, 2);
+        if (nA > 0) {
+            if (nA & 1) produce(nA, 1, ra, rb, -1, 1);
+            else produce(nA, 0, ra, rb, -1, 1);
         }
+        if constexpr (Q2) run(nA, nB, e1, 2);
         for (int k = max(0, n_ent - kQStages); k < n_ent; ++k) nb_sync(5 + (k & (kQStages - 1)), kNT);   // drain
     } else {
         // ------------------------------ consumer ------------------------------
@@ -783,18 +779,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             consume(k, 0, false);
             if (k + 1 < nA) consume(k + 1, 1, false);
         }
-        if constexpr (!BORDER) {
-#pragma unroll
-            for (int r = 0; r < kQSeg; ++r)
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
-                    if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
-                    const unsigned long long key =
-                        ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
-                    atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
-                }
-        } else {
+        {
             if (nA > 0) {
                 if (nA & 1) consume(nA, 1, true);
                 else consume(nA, 0, true);

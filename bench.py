@@ -55,8 +55,8 @@ def parse():
     ap.add_argument("--sequences", action="store_true",
                     help="independent sequences: rank r runs sequence s = r of the config on the whole frame "
                          "(SURVEY.md 8(e) mode (i), config 5's batch; weak scaling, no collective in the step)")
-    ap.add_argument("--sequential-pairs", dest="concurrent_pairs", action="store_false",
-                    help="run the three pairs of a step in order on one stream (default: one stream per pair)")
+    ap.add_argument("--no-concurrent", action="store_true",
+                    help="skip the extra timed loop with the three pairs of a step on three streams")
     return ap.parse_args()
 
 
@@ -153,6 +153,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    args.concurrent_pairs = False   # step() schedule; the timed region runs the pairs in order
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
@@ -234,10 +235,11 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     qs.qs_profile_reset()
-    # Per-launch kernel timing (qs_profile: CUDA events on each launch's stream) is taken in the timed
-    # region when the pairs run in order; with concurrent pairs the launches overlap, so the
-    # per-kernel numbers come from a sequential pass over the same steps right after it.
-    qs.qs_profile_enable(not args.concurrent_pairs)
+    # The timed region runs the pairs of a step in order on one stream, so qs_profile's per-launch CUDA
+    # events (on each launch's stream) time each kernel alone; a second timed loop over the same steps
+    # with the three pairs on three streams is reported beside it ("concurrent_pairs").
+    args.concurrent_pairs = False
+    qs.qs_profile_enable(True)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         if world > 1:
@@ -252,19 +254,30 @@ def run_ours(args):
             dist.barrier()
     qs.qs_profile_enable(False)
     ms = t0.elapsed_time(t1)
-    launches = sum(n for _, n in (qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS))
-    if args.concurrent_pairs:
-        args.concurrent_pairs = False
-        qs.qs_profile_reset()
-        qs.qs_profile_enable(True)
+    prof = {k: qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS}
+    launches = sum(n for _, n in prof.values())
+    conc = None
+    if not args.no_concurrent:
+        args.concurrent_pairs = True
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        c0.record()
         for t in order[args.warmup:]:
             step(t)
+        c1.record()
         torch.cuda.synchronize()
-        qs.qs_profile_enable(False)
-        args.concurrent_pairs = True
-    prof = {k: qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS}
-    if args.concurrent_pairs:   # the same steps launch the same kernels in either order
-        launches = sum(n for _, n in prof.values())
+        cms = c0.elapsed_time(c1)
+        if world > 1:
+            tt = torch.tensor([cms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            cms = float(tt.item())
+        n_seq_c = world if args.sequences else 1
+        conc = {"value": round(n_seq_c * args.steps * W * H / (cms / 1e3) / 1e6, 3), "unit": "Mpixel/s",
+                "ms_per_step": round(cms / args.steps, 4),
+                "how": "same steps, the three pairs on three streams (PR in order on the main stream)"}
+        args.concurrent_pairs = False
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -308,12 +321,11 @@ def run_ours(args):
                           "mask": "dynamic" if cfg.dynamic else "fixed", "check": args.check,
                           "parallelism": (f"sequences{world}" if args.sequences else f"rowband{world}") if world > 1
                           else "single",
-                          "pairs": "3 streams (one per reference d; PR in order)" if args.concurrent_pairs else "in order",
-                          "kernel_timing": "sequential pass over the same steps" if args.concurrent_pairs else "timed region",
+                          "pairs": "in order on one stream (see concurrent_pairs for three streams)",
                           "l2": f"{args.frames} resident frames (~{args.frames * W * H * (6 if f32 else 3) / 1e6:.0f} MB vs "
                                 f"126 MB L2); consecutive steps use disjoint frames"},
                "roofline": roofline, "kernel_ms_per_step": kernel_ms, "gpu_launches": launches,
-               "clocks": clk.summary(), "e2e": e2e, "impl": "ours"}
+               "clocks": clk.summary(), "e2e": e2e, "concurrent_pairs": conc, "impl": "ours"}
         if args.variants:
             out["cc_variants_ms_per_frame"] = run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

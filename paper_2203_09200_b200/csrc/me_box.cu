@@ -501,6 +501,12 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     if (n_ent <= 0) return;                              // uniform
 
     if constexpr (!BORDER) {
+        // Keyed argmin (uint8 SAD): every interior sum is an integer <= 25 * 255, so with the block
+        // values scaled by 2^9 and the candidate's chunk-list position k (< 2^9, rank order) added
+        // once per window, E' = 512 E + k is exact in fp32 (< 2^24) and orders (E, rank) exactly
+        // (R7): the running argmin is one FMNMX per output instead of compare + two selects.
+        constexpr bool KEYED = EXACT && !SSD;
+        constexpr float kKeyScale = KEYED ? 512.f : 1.f;
         // ------------------- interior: warp-specialised registers -------------------
         // Producers: two warp pairs; pair p = (warp >> 1) reduces the candidates k = p, p + 2, ...
         // into ring stage p, warp half = warp & 1 of a pair takes H columns 16 half .. +15 (20 blocks
@@ -523,7 +529,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 const int q = m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
                 const int dy = q >> 1, dx = q & 1;
                 cv[kk] = (float)a.cur.p[(r + dy) * a.cur.pitch + x + dx];
-                wy2[kk] = f2pack((float)(1 - dy), (float)dy);
+                wy2[kk] = f2pack(kKeyScale * (float)(1 - dy), kKeyScale * (float)dy);   // x 2^9 when keyed
                 wx[kk] = (float)dx;
                 ad[kk] = 4 * (dy * bplane + (bi + 2) * bpitch + (2 * bk + dx + 4 + a.S));
             }
@@ -585,14 +591,20 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 nb_arrive_i<5 + P, kQBarI>();                           // EMPTY[P]
                 f2_t pp0 = f2add(x[0], x[1]), pp1 = f2add(x[1], x[2]), pp2 = f2add(x[2], x[3]);
                 f2_t pp3 = f2add(x[3], x[4]);
+                // keyed: (k, 0) added to every V, so each E (one lo + one hi) carries k exactly once
+                const f2_t kk2 = f2pack(KEYED ? (float)k : 0.f, 0.f);
                 f2_t vcur = f2add(pp0, pp2);
+                if constexpr (KEYED) vcur = f2add(vcur, kk2);
 #pragma unroll
                 for (int r = 0; r < kQSeg; ++r) {
-                    const f2_t vnext = f2add(pp1, pp3);
+                    f2_t vnext = f2add(pp1, pp3);
+                    if constexpr (KEYED) vnext = f2add(vnext, kk2);
                     const float ev[2] = {__fadd_rn(f2lo(vcur), f2hi(vcur)), __fadd_rn(f2hi(vcur), f2lo(vnext))};
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
-                        if (ev[c] < be[r][c]) { be[r][c] = ev[c]; br[r][c] = rank; }
+                    for (int c = 0; c < 2; ++c) {
+                        if constexpr (KEYED) be[r][c] = fminf(be[r][c], ev[c]);
+                        else if (ev[c] < be[r][c]) { be[r][c] = ev[c]; br[r][c] = rank; }
+                    }
                     vcur = vnext;
                     pp0 = pp1;
                     pp1 = pp2;
@@ -609,6 +621,12 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
+                    if constexpr (KEYED) {
+                        if (!(be[r][c] < INFINITY)) continue;
+                        const unsigned kv = (unsigned)be[r][c];           // 512 E + k, exact
+                        br[r][c] = clist[kv & 511u] >> 16;
+                        be[r][c] = (float)(kv >> 9);
+                    }
                     if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
                     const unsigned long long key =
                         ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];

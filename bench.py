@@ -55,8 +55,12 @@ def parse():
     ap.add_argument("--sequences", action="store_true",
                     help="independent sequences: rank r runs sequence s = r of the config on the whole frame "
                          "(SURVEY.md 8(e) mode (i), config 5's batch; weak scaling, no collective in the step)")
-    ap.add_argument("--no-concurrent", action="store_true",
-                    help="skip the extra timed loop with the three pairs of a step on three streams")
+    ap.add_argument("--pairs", default="refs", choices=["refs", "in_order", "streams"],
+                    help="how a step runs its three (frame, reference) pairs: refs = one qs_me_search_refs call "
+                         "(one launch per kernel for the three references; default), in_order = three "
+                         "qs_me_search calls on one stream, streams = three calls on three streams")
+    ap.add_argument("--no-compare", action="store_true",
+                    help="skip the extra timed loop that runs the same steps as three in-order qs_me_search calls")
     return ap.parse_args()
 
 
@@ -153,7 +157,6 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    args.concurrent_pairs = False   # step() schedule; the timed region runs the pairs in order
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
@@ -192,18 +195,26 @@ def run_ours(args):
     checks = qs.make_checks() if args.check == "nnc_frmc" else None
     fields = [qs.Field.alloc(band.rows, W, f32, dev) for _ in range(3)]
     wss = [qs.workspace(roi, prm, dev) for _ in range(3)]
+    ws3 = qs.workspace(roi, prm, dev, n_refs=3)
     acc_s, acc_c = qs.alloc_acc(band.rows, W, dev)
     evals = torch.zeros(1, dtype=torch.int64, device=dev)
 
     main = torch.cuda.current_stream(dev)
     pair_streams = [torch.cuda.Stream(dev) for _ in range(3)]
 
-    def step(t):
+    def step(t, mode):
         if banded:
             rowband.exchange_halo(dfr[t - 1]["ref"], band)
         acc_s.zero_()
         acc_c.zero_()
-        if not args.concurrent_pairs:
+        if mode == "refs":       # ME + checks of the three pairs: one launch per kernel
+            fr = dfr[t]
+            qs.qs_me_search_refs(fr["cur"], fr["mask"], [dfr[t - d]["ref"] for d in (1, 2, 3)], roi, prm, fields,
+                                 fuse=checks, eval_count=evals, ws=ws3)
+            for d in (1, 2, 3):
+                qs.qs_project(fields[d - 1], dfr[t - d]["cur"], dfr[t - d]["mask"], roi, acc_s, acc_c)
+            return
+        if mode == "in_order":
             for d in (1, 2, 3):
                 fr, past = dfr[t], dfr[t - d]
                 qs.qs_me_search(fr["cur"], fr["mask"], past["ref"], roi, prm, fields[d - 1], fuse=checks,
@@ -229,16 +240,17 @@ def run_ours(args):
             qs.qs_project(fields[d - 1], dfr[t - d]["cur"], dfr[t - d]["mask"], roi, acc_s, acc_c)
 
     order = step_order(args.frames, args.warmup + args.steps)
+    cmp_mode = None if args.no_compare else ("in_order" if args.pairs != "in_order" else "refs")
     for t in order[:args.warmup]:
-        step(t)
+        step(t, args.pairs)
+        if cmp_mode:
+            step(t, cmp_mode)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     qs.qs_profile_reset()
-    # The timed region runs the pairs of a step in order on one stream, so qs_profile's per-launch CUDA
-    # events (on each launch's stream) time each kernel alone; a second timed loop over the same steps
-    # with the three pairs on three streams is reported beside it ("concurrent_pairs").
-    args.concurrent_pairs = False
+    # The timed region: qs_profile's per-launch CUDA events are recorded on each launch's stream, so
+    # in the refs and in_order modes (one stream) they time each kernel alone inside the timed region.
     qs.qs_profile_enable(True)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -247,7 +259,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0.record()
         for t in order[args.warmup:]:
-            step(t)
+            step(t, args.pairs)
         t1.record()
         torch.cuda.synchronize()
         if world > 1:
@@ -257,15 +269,14 @@ def run_ours(args):
     prof = {k: qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS}
     launches = sum(n for _, n in prof.values())
     conc = None
-    if not args.no_concurrent:
-        args.concurrent_pairs = True
+    if cmp_mode:
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         c0.record()
         for t in order[args.warmup:]:
-            step(t)
+            step(t, cmp_mode)
         c1.record()
         torch.cuda.synchronize()
         cms = c0.elapsed_time(c1)
@@ -274,10 +285,9 @@ def run_ours(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             cms = float(tt.item())
         n_seq_c = world if args.sequences else 1
-        conc = {"value": round(n_seq_c * args.steps * W * H / (cms / 1e3) / 1e6, 3), "unit": "Mpixel/s",
-                "ms_per_step": round(cms / args.steps, 4),
-                "how": "same steps, the three pairs on three streams (PR in order on the main stream)"}
-        args.concurrent_pairs = False
+        conc = {"pairs": cmp_mode, "value": round(n_seq_c * args.steps * W * H / (cms / 1e3) / 1e6, 3),
+                "unit": "Mpixel/s", "ms_per_step": round(cms / args.steps, 4),
+                "how": "same steps, timed the same way, with the other pair schedule"}
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -289,7 +299,8 @@ def run_ours(args):
     me_ms, me_n = prof["me_box"]
     n_cand = (2 * S + 1) ** 2
     me_rows = min(H, band.y1 + 2) - max(0, band.y0 - 2)
-    units_per_launch = me_rows * W * n_cand
+    # (pixel, candidate) units of the timed region (3 pairs per step) per me_box launch
+    units_per_launch = (args.steps * 3 * me_rows * W * n_cand) // me_n if me_n else 0
     achieved = OPS_PER_UNIT * units_per_launch / (me_ms / me_n / 1e3) / 1e12 if me_n else None
     peak = SM_COUNT * FP32_LANES_PER_SM * SM_MAX_MHZ * 1e6 / 1e12
     traffic = None
@@ -321,11 +332,14 @@ def run_ours(args):
                           "mask": "dynamic" if cfg.dynamic else "fixed", "check": args.check,
                           "parallelism": (f"sequences{world}" if args.sequences else f"rowband{world}") if world > 1
                           else "single",
-                          "pairs": "in order on one stream (see concurrent_pairs for three streams)",
+                          "pairs": {"refs": "one qs_me_search_refs call per step (one launch per kernel for "
+                                            "the three references)",
+                                    "in_order": "three qs_me_search calls in order on one stream",
+                                    "streams": "three qs_me_search calls on three streams"}[args.pairs],
                           "l2": f"{args.frames} resident frames (~{args.frames * W * H * (6 if f32 else 3) / 1e6:.0f} MB vs "
                                 f"126 MB L2); consecutive steps use disjoint frames"},
                "roofline": roofline, "kernel_ms_per_step": kernel_ms, "gpu_launches": launches,
-               "clocks": clk.summary(), "e2e": e2e, "concurrent_pairs": conc, "impl": "ours"}
+               "clocks": clk.summary(), "e2e": e2e, "compare": conc, "impl": "ours"}
         if args.variants:
             out["cc_variants_ms_per_frame"] = run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -357,6 +371,7 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
     sets = [slot_set(), slot_set()]
     fields = [qs.Field.alloc(band.rows, W, f32, dev) for _ in range(3)]
     wss = [qs.workspace(roi, prm, dev) for _ in range(3)]
+    ws3 = qs.workspace(roi, prm, dev, n_refs=3)
     acc_s, acc_c = qs.alloc_acc(band.rows, W, dev)
     out_s = torch.empty((band.rows, W), dtype=torch.int32).pin_memory()
     out_c = torch.empty((band.rows, W), dtype=torch.uint8).pin_memory()
@@ -392,7 +407,12 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
                 ready_next = issue_copies(i + 1, ts, done[(i + 1) % 2])
             acc_s.zero_()
             acc_c.zero_()
-            if args.concurrent_pairs:
+            if args.pairs == "refs":
+                qs.qs_me_search_refs(slots[0]["cur"], slots[0]["mask"], [slots[d]["ref"] for d in (1, 2, 3)], roi,
+                                     prm, fields, fuse=checks, ws=ws3)
+                for d in (1, 2, 3):
+                    qs.qs_project(fields[d - 1], slots[d]["cur"], slots[d]["mask"], roi, acc_s, acc_c)
+            elif args.pairs == "streams":
                 start = torch.cuda.Event()
                 start.record(comp)
                 pev = []

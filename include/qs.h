@@ -177,6 +177,28 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
                  void *stream);
 
 /* ---------------------------------------------------------------------------
+ * qs_me_search_refs -- qs_me_search for the pairs (cur, refs[i]) of one frame,
+ * i = 0..n_refs-1 (the d = 1..3 references of PAPER.md:131 "the last three
+ * frames"): the same results as n_refs calls
+ * of qs_me_search(cur, cur_mask, cur_pitch, refs[i], ref_pitch, roi, p, fuse,
+ * &outs[i], ...), with ME and the fused checks of all references in ONE launch
+ * per kernel (K = 8 with the paper's FRMC offsets or no FRMC; other settings run
+ * the calls one by one).  The template statics of the current frame are shared
+ * by the references' CTAs, which run side by side (no per-reference tail).
+ *
+ *   refs        HOST array of n_refs DEVICE reference planes (same type, pitch)
+ *   outs        HOST array of n_refs fields (each with its own planes / pitch)
+ *   eval_count  nullable device counter: the sum over the references
+ *   workspace   n_refs slots of qs_workspace_size() bytes each
+ * n_refs = 0 is a no-op; any n_refs >= 1 is accepted (launched in groups of 4).
+ * Errors as qs_me_search; a failing group leaves later references untouched.
+ * ------------------------------------------------------------------------- */
+int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, int32_t n_refs,
+                      const void *const *refs, int64_t ref_pitch, const qs_roi *roi, const qs_me_params *p,
+                      const qs_checks *fuse, qs_field *outs, unsigned long long *eval_count, void *workspace,
+                      size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
  * qs_reverse_check -- the literature's RME (mode QS_RME; PAPER.md:71-72:
  * "the motion vectors in the reverse direction are calculated using an
  * additional reverse motion estimation (RME). Only when both motion vectors

@@ -77,12 +77,14 @@ def lib() -> C.CDLL:
         L.qs_workspace_size.argtypes = [P(qs_roi), i32, i32, P(qs_me_params), P(sz)]
         L.qs_me_search.argtypes = [vp, vp, i64, vp, i64, P(qs_roi), P(qs_me_params), P(qs_checks), P(qs_field),
                                    vp, vp, sz, vp]
+        L.qs_me_search_refs.argtypes = [vp, vp, i64, i32, vp, i64, P(qs_roi), P(qs_me_params), P(qs_checks),
+                                        vp, vp, vp, sz, vp]
         L.qs_reverse_check.argtypes = [i32, vp, vp, i64, vp, i64, P(qs_roi), P(qs_me_params), P(qs_field),
                                        vp, vp, sz, vp]
         L.qs_frmc.argtypes = [vp, vp, i64, vp, i64, P(qs_roi), P(qs_me_params), vp, i32, P(qs_field), vp, vp]
         L.qs_nnc.argtypes = [P(qs_field), P(qs_roi), i32, vp]
         L.qs_project.argtypes = [P(qs_field), vp, vp, i64, P(qs_roi), vp, vp, i64, vp]
-        for f in ("qs_workspace_size", "qs_me_search", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_project"):
+        for f in ("qs_workspace_size", "qs_me_search", "qs_me_search_refs", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_project"):
             getattr(L, f).restype = C.c_int
         L.qs_profile_enable.argtypes = [i32]
         L.qs_profile_read.argtypes = [C.c_char_p, P(C.c_double), P(C.c_int64)]
@@ -223,8 +225,30 @@ def qs_workspace_size(roi: qs_roi, params: qs_me_params) -> int:
     return n.value
 
 
-def workspace(roi: qs_roi, params: qs_me_params, device="cuda") -> torch.Tensor:
-    return torch.empty(max(qs_workspace_size(roi, params), 16), dtype=torch.uint8, device=device)
+def workspace(roi: qs_roi, params: qs_me_params, device="cuda", n_refs: int = 1) -> torch.Tensor:
+    """Device scratch for qs_me_search (n_refs = 1) or qs_me_search_refs (n_refs slots)."""
+    return torch.empty(max(qs_workspace_size(roi, params) * max(n_refs, 1), 16), dtype=torch.uint8, device=device)
+
+
+def qs_me_search_refs(cur, cur_mask, refs, roi: qs_roi, params: qs_me_params, outs, fuse: qs_checks | None = None,
+                      eval_count: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """qs_me_search for the pairs (cur, refs[i]) -> outs[i] of one frame in one launch per kernel."""
+    if _pitch_bytes(cur) != _pitch_bytes(cur_mask):
+        raise ValueError("cur and cur_mask must share one pitch")
+    n = len(refs)
+    if len(outs) != n:
+        raise ValueError("refs and outs differ in length")
+    pitches = {_pitch_bytes(r) for r in refs}
+    if len(pitches) > 1:
+        raise ValueError("reference planes must share one pitch")
+    if ws is None:
+        ws = workspace(roi, params, cur.device, n)
+    rp = (C.c_void_p * max(n, 1))(*[r.data_ptr() for r in refs])
+    fc = (qs_field * max(n, 1))(*[o.c() for o in outs])
+    _check(lib().qs_me_search_refs(_ptr(cur), _ptr(cur_mask), _pitch_bytes(cur), n, C.cast(rp, C.c_void_p),
+                                   pitches.pop() if pitches else 16, C.byref(roi), C.byref(params),
+                                   C.byref(fuse) if fuse is not None else None, C.cast(fc, C.c_void_p),
+                                   _ptr(eval_count), _ptr(ws), ws.numel(), _stream(stream)))
 
 
 def qs_me_search(cur, cur_mask, ref, roi: qs_roi, params: qs_me_params, out: Field, fuse: qs_checks | None = None,

@@ -57,8 +57,10 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
     const int tx0 = blockIdx.x * kFT, ty0 = g.lo + blockIdx.y * kFT;
     const tile::Regions R = tile::layout(sm, ty0, tx0, 7, g.S, g.W, g.H);
     const int tid = threadIdx.x;
+    const int zr = blockIdx.z;                   // reference slot (qs_me_search_refs)
+    const unsigned long long *keys = g.keys_p[zr];
     if (tid == 0) S.n_ent = 0;
-    tile::stage<F32>(R, g.cur, g.mask, g.ref, g.W, g.H, g.buf_y0, g.buf_rows);
+    tile::stage<F32>(R, g.cur, g.mask, Plane{g.ref_p[zr], g.ref.pitch}, g.W, g.H, g.buf_y0, g.buf_rows);
 
     // 1. Decode the vectors of the tile + 2-pixel halo from the keys; validity needs the
     //    support n of the chosen vector (min_support, R6), counted from the mask bits.
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
             const bool measured = (tile::mask_bits(R, cr, cc) & 1u) != 0;
             if (!measured) {
                 st0 = kInvalid;
-                const unsigned long long key = g.keys[(int64_t)(gy - g.lo) * g.key_pitch + gx];
+                const unsigned long long key = keys[(int64_t)(gy - g.lo) * g.key_pitch + gx];
                 if (key != ~0ull) {
                     const int pk = __ldg(g.canon + (int)(key & 0xffffffffu));
                     const int a = (int)(int8_t)(pk & 0xff), b = (int)(int8_t)((pk >> 8) & 0xff);
@@ -184,14 +186,14 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
         }
     }
     if (own) {
-        const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f.pitch + gx;
+        const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f_p[zr].pitch + gx;
         const bool has = st >= kCandidate;
-        g.f.alpha[fi] = has ? (int8_t)a : (int8_t)0;
-        g.f.beta[fi] = has ? (int8_t)b : (int8_t)0;
-        g.f.count[fi] = has ? S.n0[tid] : (uint8_t)0;
-        if (F32) reinterpret_cast<float *>(g.f.err)[fi] = has ? ef : 0.f;
-        else reinterpret_cast<uint32_t *>(g.f.err)[fi] = has ? eu : 0u;
-        if (!FRMC) g.f.status[fi] = st;
+        g.f_p[zr].alpha[fi] = has ? (int8_t)a : (int8_t)0;
+        g.f_p[zr].beta[fi] = has ? (int8_t)b : (int8_t)0;
+        g.f_p[zr].count[fi] = has ? S.n0[tid] : (uint8_t)0;
+        if (F32) reinterpret_cast<float *>(g.f_p[zr].err)[fi] = has ? ef : 0.f;
+        else reinterpret_cast<uint32_t *>(g.f_p[zr].err)[fi] = has ? eu : 0u;
+        if (!FRMC) g.f_p[zr].status[fi] = st;
     }
     if (!FRMC) return;
 
@@ -222,8 +224,8 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
     __syncthreads();
     if (own) {
         const bool checked = checked_row && (st == kCandidate || st == kAccepted);
-        const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f.pitch + gx;
-        g.f.status[fi] = checked ? (S.rej[tid] ? kRejected : kAccepted) : st;
+        const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f_p[zr].pitch + gx;
+        g.f_p[zr].status[fi] = checked ? (S.rej[tid] ? kRejected : kAccepted) : st;
     }
     if (g.evals && tid == 0 && ne) atomicAdd(g.evals, 49ull * (unsigned long long)ne);
 }
@@ -234,7 +236,7 @@ cudaError_t launch_epi_t(const EpiArgs &g, cudaStream_t s) {
     auto fn = epilogue_kernel<SSD, F32, NNC, FRMC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grd((g.W + kFT - 1) / kFT, (g.hi - g.lo + kFT - 1) / kFT);
+    dim3 grd((g.W + kFT - 1) / kFT, (g.hi - g.lo + kFT - 1) / kFT, g.n_ref);
     fn<<<grd, 256, smem, s>>>(g);
     return cudaGetLastError();
 }
@@ -249,8 +251,16 @@ cudaError_t launch_epi_c(const EpiArgs &g, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t launch_epilogue(const EpiArgs &g, cudaStream_t s) {
-    if (g.hi <= g.lo) return cudaSuccess;
+cudaError_t launch_epilogue(const EpiArgs &g0, cudaStream_t s) {
+    if (g0.hi <= g0.lo) return cudaSuccess;
+    EpiArgs g = g0;
+    if (g.n_ref <= 0) {   // one slot: (ref, keys, f)
+        g.n_ref = 1;
+        g.ref_p[0] = g.ref.p;
+        g.keys_p[0] = g.keys;
+        g.f_p[0] = g.f;
+    }
+    if (g.n_ref > kMaxRefs) return cudaErrorInvalidValue;
     if (g.ref_f32) return g.ssd ? launch_epi_c<true, true>(g, s) : launch_epi_c<false, true>(g, s);
     return g.ssd ? launch_epi_c<true, false>(g, s) : launch_epi_c<false, false>(g, s);
 }

@@ -36,12 +36,16 @@ namespace {
 
 // B/A loaders: float value or NaN ("no term").
 // Rows outside the frame, or outside the caller's buffer window, give NaN.
+// The launch's reference slot of this CTA (qs_me_search_refs: CTA b works on slot b % n_ref).
+__device__ __forceinline__ int ref_slot(const BoxArgs &a) { return (int)(blockIdx.x % (unsigned)a.n_ref); }
+
 __device__ __forceinline__ float load_ref(const BoxArgs &a, int y, int x) {
     if (y < 0 || y >= a.H || x < 0 || x >= a.W || y < a.buf_y0 || y >= a.buf_y0 + a.buf_rows)
         return __int_as_float(0x7fc00000);
     const int64_t off = (int64_t)(y - a.buf_y0) * a.ref.pitch;
-    if (a.ref_f32) return reinterpret_cast<const float *>(a.ref.p + off)[x];
-    return (float)a.ref.p[off + x];
+    const uint8_t *rp = a.ref_p[ref_slot(a)];
+    if (a.ref_f32) return reinterpret_cast<const float *>(rp + off)[x];
+    return (float)rp[off + x];
 }
 
 __device__ __forceinline__ float load_cur_masked(const BoxArgs &a, int y, int x) {
@@ -276,7 +280,7 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
             hi = (unsigned long long)floor((double)be[i] * 8192.0 / (double)bn[i]);
         }
         const unsigned long long key = (hi << 32) | (unsigned)br[i];
-        atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+        atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
     }
 }
 
@@ -630,7 +634,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                     if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
                     const unsigned long long key =
                         ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
-                    atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+                    atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
                 }
         }
         return;
@@ -760,7 +764,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             unsigned long long hi;
             if constexpr (EXACT) hi = (unsigned long long)floor((double)e * 8192.0 / (double)n);
             else hi = __float_as_uint(__fdiv_rn(e, n));
-            atomicMin(a.keys + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), (hi << 32) | (unsigned)rank);
+            atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), (hi << 32) | (unsigned)rank);
         };
         // Phase-1 entry (or the npx entry when last): E for the 28 outputs from the 18 H rows.
         auto consume = [&](int e, const int s, const bool last) {
@@ -876,7 +880,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
 template <int K, bool EXACT, bool SSD, bool REV>
 __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
     extern __shared__ __align__(16) float smem[];
-    const int unit = blockIdx.x;
+    const int unit = blockIdx.x / a.n_ref;   // the slots of one unit run side by side
     const int chunk = unit % a.n_chunks;
     const int tile = unit / a.n_chunks;
     const int txi = tile % a.tiles_x;
@@ -931,7 +935,7 @@ cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
     auto fn = box_kernel<K, EXACT, SSD, REV>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const long long units = (long long)a.tiles_x * a.tiles_y * a.n_chunks;
+    const long long units = (long long)a.tiles_x * a.tiles_y * a.n_chunks * a.n_ref;
     if (units <= 0) return cudaSuccess;
     fn<<<(unsigned)units, kNT, smem, s>>>(a);
     return cudaGetLastError();
@@ -1015,7 +1019,14 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
 
 }  // namespace
 
-cudaError_t launch_box(const BoxArgs &a, int K, bool ssd, bool reverse, cudaStream_t s) {
+cudaError_t launch_box(const BoxArgs &a0, int K, bool ssd, bool reverse, cudaStream_t s) {
+    BoxArgs a = a0;
+    if (a.n_ref <= 0) {   // one slot: (ref, keys)
+        a.n_ref = 1;
+        a.ref_p[0] = a.ref.p;
+        a.keys_p[0] = a.keys;
+    }
+    if (a.n_ref > kMaxRefs || (reverse && a.n_ref != 1)) return cudaErrorInvalidValue;
     switch (K) {
         case 1: return launch_k<1>(a, ssd, reverse, s);
         case 2: return launch_k<2>(a, ssd, reverse, s);

@@ -435,6 +435,117 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     return QS_OK;
 }
 
+int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, int32_t n_refs,
+                      const void *const *refs, int64_t ref_pitch, const qs_roi *roi, const qs_me_params *p,
+                      const qs_checks *fuse, qs_field *outs, unsigned long long *eval_count, void *workspace,
+                      size_t workspace_bytes, void *stream) {
+    Roi r;
+    int rc;
+    if (n_refs < 0) return fail(QS_EINVAL, "n_refs=%d", n_refs);
+    if (n_refs > 0 && (!refs || !outs)) return fail(QS_EINVAL, "refs / outs is NULL");
+    if ((rc = check_roi(roi, &r)) || (rc = check_params(p))) return rc;
+    size_t slot = 0;
+    if ((rc = qs_workspace_size(roi, r.W, r.H, p, &slot))) return rc;
+    if (n_refs == 0) return QS_OK;
+    if (!workspace || !aligned16(workspace) || workspace_bytes < slot * (size_t)n_refs)
+        return fail(QS_EDIM, "workspace: need %zu bytes (%d slots of %zu, 16-byte aligned), got %zu",
+                    slot * (size_t)n_refs, n_refs, slot, workspace_bytes);
+    char *ws = static_cast<char *>(workspace);
+    const bool nnc = fuse && fuse->nnc, frmc = fuse && fuse->frmc;
+    const bool paper = frmc && is_paper_offsets(fuse->offsets, fuse->n_offsets);
+    // The single-launch path covers the fused K = 8 epilogue; everything else runs slot by slot.
+    if (p->K_h != 8 || (frmc && !paper)) {
+        for (int i = 0; i < n_refs; ++i)
+            if ((rc = qs_me_search(cur, cur_mask, cur_pitch, refs[i], ref_pitch, roi, p, fuse, &outs[i], eval_count,
+                                   ws + slot * i, slot, stream)))
+                return rc;
+        return QS_OK;
+    }
+    for (int i0 = 0; i0 < n_refs; i0 += kMaxRefs) {   // groups of kMaxRefs slots per launch
+        const int n = std::min(n_refs - i0, kMaxRefs);
+        const int esz = p->ref_type == QS_REF_F32 ? 4 : 1;
+        if ((rc = check_plane(cur, cur_pitch, r.W, "cur")) || (rc = check_plane(cur_mask, cur_pitch, r.W, "cur_mask")))
+            return rc;
+        for (int i = 0; i < n; ++i)
+            if ((rc = check_plane(refs[i0 + i], ref_pitch, (int64_t)r.W * esz, "ref")) ||
+                (rc = check_field(&outs[i0 + i], r.W, true)))
+                return rc;
+        if (nnc && fuse->nnc_threshold < 0) return fail(QS_EINVAL, "nnc_threshold < 0");
+        if (frmc && (rc = check_offsets(fuse->offsets, fuse->n_offsets, p->S))) return rc;
+        const int lo = nnc ? std::max(0, r.y0 - 2) : r.y0, hi = nnc ? std::min(r.H, r.y1 + 2) : r.y1;
+        const int KL = 4, KR = 3;
+        if ((rc = need_rows(r, lo, hi, "field")) || (rc = need_rows(r, lo - KL - p->S, hi + KR + p->S, "ME inputs")))
+            return rc;
+        const char *terr = nullptr;
+        const CandTables *t = cand_tables(p->S, &terr);
+        if (!t) return fail(QS_ECUDA, "%s", terr);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (r.y1 <= r.y0 || hi <= lo) return QS_OK;
+        const size_t kb = me_keys_bytes(r);
+        char *wg = ws + slot * i0;
+        // Key planes of the group's slots (slot i at wg + i * slot; one memset over the span).
+        cudaError_t e = cudaMemsetAsync(wg, 0xff, slot * (n - 1) + kb, s);
+        if (e != cudaSuccess) return cuda_fail(e, "memset keys");
+        BoxArgs a = box_args(r, cur, cur_mask, cur_pitch, refs[i0], ref_pitch, p, t);
+        a.oy0 = lo;
+        a.oy1 = hi;
+        a.ox0 = 0;
+        a.ox1 = r.W;
+        a.tiles_x = (r.W + kTX - 1) / kTX;
+        a.tiles_y = (hi - lo + kTY - 1) / kTY;
+        a.keys = reinterpret_cast<unsigned long long *>(wg);
+        a.key_pitch = r.W;
+        a.n_ref = n;
+        for (int i = 0; i < n; ++i) {
+            a.ref_p[i] = static_cast<const uint8_t *>(refs[i0 + i]);
+            a.keys_p[i] = reinterpret_cast<unsigned long long *>(wg + slot * i);
+        }
+        {
+            ProfScope ps(P_ME_BOX, s);
+            e = launch_box(a, 8, p->err == QS_SSD, false, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "me_box launch");
+        EpiArgs g{};
+        g.cur = a.cur;
+        g.mask = a.mask;
+        g.ref = a.ref;
+        g.ref_f32 = a.ref_f32;
+        g.ssd = p->err == QS_SSD;
+        g.W = r.W;
+        g.H = r.H;
+        g.buf_y0 = r.b0;
+        g.buf_rows = r.br;
+        g.S = p->S;
+        g.min_support = p->min_support;
+        g.lo = lo;
+        g.hi = hi;
+        g.y0 = r.y0;
+        g.y1 = r.y1;
+        g.keys = a.keys;
+        g.key_pitch = r.W;
+        g.canon = t->canon;
+        g.f = view(&outs[i0]);
+        g.nnc = nnc;
+        g.nnc_threshold = nnc ? fuse->nnc_threshold : 0;
+        g.frmc = paper;
+        const int8_t order[7] = {0, -1, 1, -3, 3, -7, 7};
+        for (int i = 0; paper && i < 7; ++i) g.dys[i] = order[i];
+        g.evals = eval_count;
+        g.n_ref = n;
+        for (int i = 0; i < n; ++i) {
+            g.ref_p[i] = a.ref_p[i];
+            g.keys_p[i] = a.keys_p[i];
+            g.f_p[i] = view(&outs[i0 + i]);
+        }
+        {
+            ProfScope ps(P_EPILOGUE, s);
+            e = launch_epilogue(g, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "epilogue launch");
+    }
+    return QS_OK;
+}
+
 int qs_reverse_check(int32_t mode, const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, const void *ref,
                      int64_t ref_pitch, const qs_roi *roi, const qs_me_params *p, qs_field *io,
                      unsigned long long *eval_count, void *workspace, size_t workspace_bytes, void *stream) {

@@ -58,8 +58,12 @@ struct Plane {
 };
 
 // Arguments of the box kernels (forward ME and dense reverse ME).
+// References per launch: qs_me_search_refs runs the pairs (cur, ref_i) of one frame in a single
+// launch per kernel; slot i's reference plane, key plane and field.
+constexpr int kMaxRefs = 4;
+
 struct BoxArgs {
-    Plane cur, mask, ref;
+    Plane cur, mask, ref;            // ref.p == ref_p[0]; ref.pitch is shared by every slot
     int ref_f32;
     int W, H, buf_y0, buf_rows;
     int S, min_support;
@@ -67,8 +71,11 @@ struct BoxArgs {
     int tiles_x, tiles_y, n_chunks;
     const int32_t *chunked;
     const int32_t *chunk_off;
-    unsigned long long *keys;        // [oy1-oy0][key_pitch]
+    unsigned long long *keys;        // [oy1-oy0][key_pitch] (slot 0)
     int64_t key_pitch;
+    int n_ref;                       // slots per launch: CTA b works on slot b % n_ref (0 -> 1)
+    const uint8_t *ref_p[kMaxRefs];
+    unsigned long long *keys_p[kMaxRefs];
 };
 
 // Launchers (me_box.cu).  Return cudaError_t of the launch.
@@ -115,6 +122,10 @@ struct EpiArgs {
     int nnc, nnc_threshold, frmc;
     int8_t dys[8];                   // FRMC delta_y order (a permutation of the paper's offsets)
     unsigned long long *evals;
+    int n_ref;                       // slots per launch (grid z); 0 -> 1 with slot 0 = (ref, keys, f)
+    const uint8_t *ref_p[kMaxRefs];
+    const unsigned long long *keys_p[kMaxRefs];
+    FieldView f_p[kMaxRefs];
 };
 cudaError_t launch_epilogue(const EpiArgs &g, cudaStream_t s);
 

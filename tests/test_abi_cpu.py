@@ -21,7 +21,7 @@ def lib():
 
 def test_exports_every_header_symbol(lib):
     names = qs.header_functions()
-    assert set(names) >= {"qs_me_search", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_project",
+    assert set(names) >= {"qs_me_search", "qs_me_search_refs", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_project",
                           "qs_last_error", "qs_workspace_size", "qs_version"}
     for n in names:
         assert hasattr(lib, n), n
@@ -87,3 +87,23 @@ def test_other_entry_points_validate(lib):
     arr = (C.c_int8 * 2)(0, 1)
     assert lib.qs_frmc(C.c_void_p(FAKE), C.c_void_p(FAKE), 64, C.c_void_p(FAKE), 64, C.byref(roi), C.byref(prm),
                        C.cast(arr, C.c_void_p), 0, C.byref(f), None, None) == qs.QS_EINVAL
+
+
+def test_me_search_refs_validates(lib):
+    roi = qs.make_roi(64, 64)
+    prm = qs.make_params(K=8, S=8)
+    slot = qs.qs_workspace_size(roi, prm)
+    refs = (C.c_void_p * 3)(FAKE, FAKE, FAKE)
+    outs = (qs.qs_field * 3)(_field(), _field(), _field())
+
+    def call(n, wsb, cur=FAKE, r=refs):
+        return lib.qs_me_search_refs(C.c_void_p(cur), C.c_void_p(cur), 64, n, C.cast(r, C.c_void_p), 64,
+                                     C.byref(roi), C.byref(prm), None, C.cast(outs, C.c_void_p), None,
+                                     C.c_void_p(FAKE), wsb, None)
+    assert call(-1, 3 * slot) == qs.QS_EINVAL
+    assert call(0, 0) == qs.QS_OK                        # no references: nothing to do
+    assert call(3, 3 * slot - 1) == qs.QS_EDIM           # one slot of workspace per reference
+    assert "slots" in qs.qs_last_error()
+    assert call(3, 3 * slot, cur=FAKE + 4) == qs.QS_EALIGN
+    bad = (C.c_void_p * 3)(FAKE, FAKE + 8, FAKE)
+    assert call(3, 3 * slot, r=bad) == qs.QS_EALIGN      # every reference plane is checked

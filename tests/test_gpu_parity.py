@@ -368,3 +368,76 @@ def test_frmc_extended_offsets(f32):
     st, ev = gpu_check("frmc", inp, o, K=8, S=S, offsets=offs)
     ost, oev = oracle.frmc(inp["cur"], inp["cur_mask"], inp["ref"], o, offsets=offs, K=8, S=S)
     assert np.array_equal(st, ost) and ev == oev
+
+
+# ---------------------------------------------------------------------------
+# qs_me_search_refs: the d = 1..3 pairs of one frame in one launch per kernel
+# ---------------------------------------------------------------------------
+def _refs_call(inps, K, S, fuse, f32):
+    H, W = inps[0]["cur"].shape
+    cur = qs.to_plane(inps[0]["cur"], DEV_)
+    msk = qs.to_plane(inps[0]["cur_mask"], DEV_)
+    refs = [qs.to_plane(i["ref"], DEV_) for i in inps]
+    roi = qs.make_roi(W, H)
+    prm = qs.make_params(K=K, S=S, ref_f32=f32)
+    outs = [qs.Field.alloc(H, W, f32, DEV_) for _ in inps]
+    ev = torch.zeros(1, dtype=torch.int64, device=DEV_)
+    qs.qs_me_search_refs(cur, msk, refs, roi, prm, outs, fuse=fuse, eval_count=ev)
+    torch.cuda.synchronize()
+    res = []
+    for o in outs:
+        g = o.numpy()
+        if not f32:
+            g["err"] = g["err"].view(np.uint32)
+        res.append(g)
+    return res, int(ev.item())
+
+
+DEV_ = "cuda"
+
+
+def test_me_search_refs_u8_bit_exact():
+    seq = synth.make_sequence(2)
+    t = 6
+    inps = [synth.pair_inputs(seq, t, d) for d in (1, 2, 3)]
+    res, ev = _refs_call(inps, 8, 16, qs.make_checks(), False)
+    oev_sum = 0
+    for d, (g, inp) in enumerate(zip(res, inps), 1):
+        o, oev = oracle.pair_chain(inp, K=8, S=16, check="nnc_frmc")
+        assert_field_equal(g, o, what=f"refs c2 t={t} d={d}")
+        oev_sum += oev
+    assert ev == oev_sum
+
+
+def test_me_search_refs_f32_equals_single_calls():
+    seq = synth.make_sequence(4, w=256, h=224)
+    inps = [synth.pair_inputs(seq, 5, d) for d in (1, 2, 3)]
+    res, ev = _refs_call(inps, 8, 9, qs.make_checks(), True)
+    ev_sum = 0
+    for g, inp in zip(res, inps):
+        s, sev = gpu_me(inp, K=8, S=9, fuse=qs.make_checks())
+        for k in ("alpha", "beta", "count", "status"):
+            assert np.array_equal(g[k], s[k]), k
+        assert np.array_equal(g["err"].view(np.uint32), s["err"].view(np.uint32))
+        ev_sum += sev
+    assert ev == ev_sum
+
+
+def test_me_search_refs_groups_and_fallback():
+    # 5 references -> two launches (groups of 4); K = 9 -> the slot-by-slot path; n_refs = 0 -> no-op
+    seq = synth.make_sequence(1)
+    inps = [synth.pair_inputs(seq, 2, d) for d in (1, 2, 1, 2, 1)]
+    res, ev = _refs_call(inps, 8, 8, qs.make_checks(), False)
+    oev_sum = 0
+    for g, inp in zip(res, inps):
+        o, oev = oracle.pair_chain(inp, K=8, S=8, check="nnc_frmc")
+        assert_field_equal(g, o, what="refs groups")
+        oev_sum += oev
+    assert ev == oev_sum
+    res9, _ = _refs_call(inps[:2], 9, 4, None, False)
+    for g, inp in zip(res9, inps[:2]):
+        o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=9, S=4)
+        assert_field_equal(g, o, what="refs K=9")
+    H, W = inps[0]["cur"].shape
+    cur = qs.to_plane(inps[0]["cur"], DEV_)
+    qs.qs_me_search_refs(cur, cur, [], qs.make_roi(W, H), qs.make_params(K=8, S=8), [])

@@ -46,6 +46,7 @@ struct EpiShared {
     int ent[kFT * kFT];
     uint8_t rej[kFT * kFT];
     uint8_t cnt8[kCW][kCW];   // measured pixels of the 8x8 current window at each region position
+    int wcnt[8];              // checkable entries per warp (the entry list is in tid = row-major order)
     int n_ent;
 };
 
@@ -59,7 +60,6 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
     const int tid = threadIdx.x;
     const int zr = blockIdx.z;                   // reference slot (qs_me_search_refs)
     const unsigned long long *keys = g.keys_p[zr];
-    if (tid == 0) S.n_ent = 0;
     tile::stage<F32>(R, g.cur, g.mask, Plane{g.ref_p[zr], g.ref.pitch}, g.W, g.H, g.buf_y0, g.buf_rows);
 
     // 1. Decode the vectors of the tile + 2-pixel halo from the keys; validity needs the
@@ -180,11 +180,10 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
         S.m0[tid] = F32 ? __fdiv_rn(ef, (float)S.n0[tid]) : 0.f;
         S.e0[tid] = F32 ? 0u : eu;
         S.rej[tid] = 0;
-        if (own && checked_row && (st == kCandidate || st == kAccepted)) {
-            const int slot = atomicAdd(&S.n_ent, 1);
-            S.ent[slot] = tid;
-        }
     }
+    const bool chk = FRMC && own && checked_row && (st == kCandidate || st == kAccepted);
+    const unsigned chk_m = __ballot_sync(0xffffffffu, chk);
+    if (FRMC && (tid & 31) == 0) S.wcnt[tid >> 5] = __popc(chk_m);
     if (own) {
         const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f_p[zr].pitch + gx;
         const bool has = st >= kCandidate;
@@ -206,6 +205,18 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
 #pragma unroll
         for (int oy = 0; oy < kFK; ++oy) n += __popc(tile::mask_bits(R, r + oy, c) & 0xffu);
         S.cnt8[r][c] = (uint8_t)n;
+    }
+    __syncthreads();
+    // Entry list in tid order (row-major in the tile): neighbouring lanes read neighbouring windows.
+    {
+        int base = 0, ne_all = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            base += (w < (tid >> 5)) ? S.wcnt[w] : 0;
+            ne_all += S.wcnt[w];
+        }
+        if (chk) S.ent[base + __popc(chk_m & ((1u << (tid & 31)) - 1u))] = tid;
+        if (tid == 0) S.n_ent = ne_all;
     }
     __syncthreads();
     const int ne = S.n_ent;

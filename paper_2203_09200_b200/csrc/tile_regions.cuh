@@ -196,16 +196,30 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
 #pragma unroll
             for (int j = 0; j < kFK; ++j) r[j] = rp[j];
             const uint32_t bits = mask_bits(g, crow + oy, ccol);
+            // Bit positions in pairs (b, b + 1): for an even offset j the two differences of a delta
+            // are one aligned FADD2 (r[ox], r[ox+1]) - (c[b], c[b+1]); per delta still ascending ox.
 #pragma unroll
-            for (int b = 0; b < kFSeg; ++b) {
-                const bool term = (bits >> b) & 1u;
+            for (int b = 0; b < kFSeg; b += 2) {
+                const bool term0 = (bits >> b) & 1u, term1 = (bits >> (b + 1)) & 1u;
 #pragma unroll
                 for (int k = 0; k < 7; ++k) {
-                    const int ox = b - pat_j<PAT>(k);
-                    if (ox < 0 || ox >= kFK) continue;
-                    const float d = __fsub_rn(r[ox], c[b]);
-                    const float t = SSD ? __fmul_rn(d, d) : fabsf(d);
-                    if (term) acc[k] = __fadd_rn(acc[k], t);
+                    const int j = pat_j<PAT>(k), ox = b - j;
+                    if ((j & 1) == 0) {
+                        if (ox < 0 || ox >= kFK) continue;
+                        float d0, d1;
+                        sub2(r[ox], r[ox + 1], c[b], c[b + 1], d0, d1);
+                        if (term0) acc[k] = __fadd_rn(acc[k], SSD ? __fmul_rn(d0, d0) : fabsf(d0));
+                        if (term1) acc[k] = __fadd_rn(acc[k], SSD ? __fmul_rn(d1, d1) : fabsf(d1));
+                    } else {
+                        if (ox >= 0 && ox < kFK) {
+                            const float d = __fsub_rn(r[ox], c[b]);
+                            if (term0) acc[k] = __fadd_rn(acc[k], SSD ? __fmul_rn(d, d) : fabsf(d));
+                        }
+                        if (ox + 1 >= 0 && ox + 1 < kFK) {
+                            const float d = __fsub_rn(r[ox + 1], c[b + 1]);
+                            if (term1) acc[k] = __fadd_rn(acc[k], SSD ? __fmul_rn(d, d) : fabsf(d));
+                        }
+                    }
                 }
             }
 #pragma unroll

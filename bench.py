@@ -209,10 +209,10 @@ def run_ours(args):
         acc_c.zero_()
         if mode == "refs":       # ME + checks of the three pairs: one launch per kernel
             fr = dfr[t]
-            qs.qs_me_search_refs(fr["cur"], fr["mask"], [dfr[t - d]["ref"] for d in (1, 2, 3)], roi, prm, fields,
-                                 fuse=checks, eval_count=evals, ws=ws3)
-            for d in (1, 2, 3):
-                qs.qs_project(fields[d - 1], dfr[t - d]["cur"], dfr[t - d]["mask"], roi, acc_s, acc_c)
+            past = [dfr[t - d] for d in (1, 2, 3)]
+            qs.qs_me_search_refs(fr["cur"], fr["mask"], [x["ref"] for x in past], roi, prm, fields,
+                                 fuse=checks, eval_count=evals, ws=ws3,
+                                 project=([x["cur"] for x in past], [x["mask"] for x in past], acc_s, acc_c))
             return
         if mode == "in_order":
             for d in (1, 2, 3):
@@ -332,8 +332,8 @@ def run_ours(args):
                           "mask": "dynamic" if cfg.dynamic else "fixed", "check": args.check,
                           "parallelism": (f"sequences{world}" if args.sequences else f"rowband{world}") if world > 1
                           else "single",
-                          "pairs": {"refs": "one qs_me_search_refs call per step (one launch per kernel for "
-                                            "the three references)",
+                          "pairs": {"refs": "one qs_me_search_refs call per step (ME, checks and PR of the "
+                                            "three references: one me_box and one epilogue launch)",
                                     "in_order": "three qs_me_search calls in order on one stream",
                                     "streams": "three qs_me_search calls on three streams"}[args.pairs],
                           "l2": f"{args.frames} resident frames (~{args.frames * W * H * (6 if f32 else 3) / 1e6:.0f} MB vs "
@@ -409,9 +409,9 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
             acc_c.zero_()
             if args.pairs == "refs":
                 qs.qs_me_search_refs(slots[0]["cur"], slots[0]["mask"], [slots[d]["ref"] for d in (1, 2, 3)], roi,
-                                     prm, fields, fuse=checks, ws=ws3)
-                for d in (1, 2, 3):
-                    qs.qs_project(fields[d - 1], slots[d]["cur"], slots[d]["mask"], roi, acc_s, acc_c)
+                                     prm, fields, fuse=checks, ws=ws3,
+                                     project=([slots[d]["cur"] for d in (1, 2, 3)],
+                                              [slots[d]["mask"] for d in (1, 2, 3)], acc_s, acc_c))
             elif args.pairs == "streams":
                 start = torch.cuda.Event()
                 start.record(comp)

@@ -188,15 +188,31 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
  *
  *   refs        HOST array of n_refs DEVICE reference planes (same type, pitch)
  *   outs        HOST array of n_refs fields (each with its own planes / pitch)
+ *   proj        NULL, or the projection PR fused into the same launch: reference i's
+ *               ACCEPTED entries project past_val[i] / past_mask[i] into sum / cnt
+ *               exactly as qs_project(&outs[i], past_val[i], past_mask[i], ...) for
+ *               i = 0..n_refs-1 would (integer sums: the result does not depend on
+ *               the order).  cnt must be 4-byte aligned with acc_pitch % 4 == 0, and
+ *               every cnt byte must stay < 256 (it does for <= 255 references on a
+ *               zeroed plane).
  *   eval_count  nullable device counter: the sum over the references
  *   workspace   n_refs slots of qs_workspace_size() bytes each
  * n_refs = 0 is a no-op; any n_refs >= 1 is accepted (launched in groups of 4).
  * Errors as qs_me_search; a failing group leaves later references untouched.
  * ------------------------------------------------------------------------- */
+typedef struct {
+    const uint8_t *const *past_val;    /* HOST array of n_refs DEVICE planes: frame t-d measurements */
+    const uint8_t *const *past_mask;   /* HOST array of n_refs DEVICE planes: their masks */
+    int64_t past_pitch;                /* bytes, shared by every past plane */
+    uint32_t *sum;                     /* [rows][acc_pitch], accumulated (caller-zeroed per frame) */
+    uint8_t *cnt;                      /* [rows][acc_pitch], accumulated */
+    int64_t acc_pitch;                 /* elements */
+} qs_projection;
+
 int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, int32_t n_refs,
                       const void *const *refs, int64_t ref_pitch, const qs_roi *roi, const qs_me_params *p,
-                      const qs_checks *fuse, qs_field *outs, unsigned long long *eval_count, void *workspace,
-                      size_t workspace_bytes, void *stream);
+                      const qs_checks *fuse, qs_field *outs, const qs_projection *proj,
+                      unsigned long long *eval_count, void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
  * qs_reverse_check -- the literature's RME (mode QS_RME; PAPER.md:71-72:

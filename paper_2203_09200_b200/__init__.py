@@ -62,6 +62,11 @@ class qs_checks(C.Structure):
                 ("offsets", C.c_void_p), ("n_offsets", C.c_int32)]
 
 
+class qs_projection(C.Structure):
+    _fields_ = [("past_val", C.c_void_p), ("past_mask", C.c_void_p), ("past_pitch", C.c_int64),
+                ("sum", C.c_void_p), ("cnt", C.c_void_p), ("acc_pitch", C.c_int64)]
+
+
 _lib = None
 
 
@@ -78,7 +83,7 @@ def lib() -> C.CDLL:
         L.qs_me_search.argtypes = [vp, vp, i64, vp, i64, P(qs_roi), P(qs_me_params), P(qs_checks), P(qs_field),
                                    vp, vp, sz, vp]
         L.qs_me_search_refs.argtypes = [vp, vp, i64, i32, vp, i64, P(qs_roi), P(qs_me_params), P(qs_checks),
-                                        vp, vp, vp, sz, vp]
+                                        vp, P(qs_projection), vp, vp, sz, vp]
         L.qs_reverse_check.argtypes = [i32, vp, vp, i64, vp, i64, P(qs_roi), P(qs_me_params), P(qs_field),
                                        vp, vp, sz, vp]
         L.qs_frmc.argtypes = [vp, vp, i64, vp, i64, P(qs_roi), P(qs_me_params), vp, i32, P(qs_field), vp, vp]
@@ -231,8 +236,12 @@ def workspace(roi: qs_roi, params: qs_me_params, device="cuda", n_refs: int = 1)
 
 
 def qs_me_search_refs(cur, cur_mask, refs, roi: qs_roi, params: qs_me_params, outs, fuse: qs_checks | None = None,
-                      eval_count: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
-    """qs_me_search for the pairs (cur, refs[i]) -> outs[i] of one frame in one launch per kernel."""
+                      eval_count: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None,
+                      project=None):
+    """qs_me_search for the pairs (cur, refs[i]) -> outs[i] of one frame in one launch per kernel.
+
+    project = (past_vals, past_masks, sum, cnt): PR of every reference fused into the same launch
+    (as qs_project(outs[i], past_vals[i], past_masks[i], roi, sum, cnt) for each i)."""
     if _pitch_bytes(cur) != _pitch_bytes(cur_mask):
         raise ValueError("cur and cur_mask must share one pitch")
     n = len(refs)
@@ -245,9 +254,25 @@ def qs_me_search_refs(cur, cur_mask, refs, roi: qs_roi, params: qs_me_params, ou
         ws = workspace(roi, params, cur.device, n)
     rp = (C.c_void_p * max(n, 1))(*[r.data_ptr() for r in refs])
     fc = (qs_field * max(n, 1))(*[o.c() for o in outs])
+    pj = None
+    if project is not None:
+        pvs, pms, acc_sum, acc_cnt = project
+        if len(pvs) != n or len(pms) != n:
+            raise ValueError("one past_val / past_mask plane per reference")
+        pp = {_pitch_bytes(x) for x in list(pvs) + list(pms)}
+        if len(pp) > 1:
+            raise ValueError("past planes must share one pitch")
+        if acc_sum.stride(0) != acc_cnt.stride(0):
+            raise ValueError("sum and cnt must share one element pitch")
+        pva = (C.c_void_p * max(n, 1))(*[x.data_ptr() for x in pvs])
+        pma = (C.c_void_p * max(n, 1))(*[x.data_ptr() for x in pms])
+        pj = qs_projection(C.cast(pva, C.c_void_p), C.cast(pma, C.c_void_p), pp.pop() if pp else 16,
+                           acc_sum.data_ptr(), acc_cnt.data_ptr(), acc_sum.stride(0))
+        pj._keep = (pva, pma)
     _check(lib().qs_me_search_refs(_ptr(cur), _ptr(cur_mask), _pitch_bytes(cur), n, C.cast(rp, C.c_void_p),
                                    pitches.pop() if pitches else 16, C.byref(roi), C.byref(params),
                                    C.byref(fuse) if fuse is not None else None, C.cast(fc, C.c_void_p),
+                                   C.byref(pj) if pj is not None else None,
                                    _ptr(eval_count), _ptr(ws), ws.numel(), _stream(stream)))
 
 

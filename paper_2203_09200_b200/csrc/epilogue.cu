@@ -47,11 +47,12 @@ struct EpiShared {
     uint8_t rej[kFT * kFT];
     uint8_t cnt8[kCW][kCW];   // measured pixels of the 8x8 current window at each region position
     int wcnt[8];              // checkable entries per warp (the entry list is in tid = row-major order)
+    uint32_t pjm[kFT * kFT], pjv[kFT * kFT];   // PR prefetch: aligned words of past_mask / past_val at p+v
     int n_ent;
 };
 
 template <bool SSD, bool F32, bool NNC, bool FRMC>
-__global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
+__global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
     extern __shared__ __align__(16) float sm[];
     __shared__ EpiShared S;
     constexpr int KL = kFK / 2;
@@ -147,6 +148,22 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
     const int a = S.sa[ly + 2][lx + 2], b = S.sb[ly + 2][lx + 2];
     float ef = 0.f;
     uint32_t eu = 0;
+    // PR prefetch (fused projection): the words holding past_mask / past_val at q = p + v, fetched
+    // with cp.async now and read after FRMC, so the gather latency hides under the checks.
+    int pj_sh = -1;
+    if (g.proj && own && checked_row && st == kCandidate) {
+        const int qy = gy + a, qx = gx + b;
+        if (qy >= 0 && qy < g.H && qx >= 0 && qx < g.W && qy >= g.buf_y0 && qy < g.buf_y0 + g.buf_rows) {
+            const int64_t qi = (int64_t)(qy - g.buf_y0) * g.past_pitch + qx;
+            const uintptr_t am = reinterpret_cast<uintptr_t>(g.pm_p[zr] + qi), av = reinterpret_cast<uintptr_t>(g.pv_p[zr] + qi);
+            pj_sh = 8 * (int)(am & 3);   // past planes share one pitch and are 16-byte aligned: same offset
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(&S.pjm[tid])),
+                         "l"(am & ~uintptr_t(3)));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(&S.pjv[tid])),
+                         "l"(av & ~uintptr_t(3)));
+        }
+    }
+    asm volatile("cp.async.commit_group;");
     if (own && st == kCandidate) {
         const int crow = (gy - KL) - R.cy0, ccol = (gx - KL) - R.cx0;
         const int rrow = (gy + a - KL) - R.ry0, rcol = (gx + b - KL) - R.rx0;
@@ -184,6 +201,20 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
     const bool chk = FRMC && own && checked_row && (st == kCandidate || st == kAccepted);
     const unsigned chk_m = __ballot_sync(0xffffffffu, chk);
     if (FRMC && (tid & 31) == 0) S.wcnt[tid >> 5] = __popc(chk_m);
+    // PR (R18) of the entries whose final status is ACCEPTED, into the frame's sum / cnt.
+    // Called by the whole warp: the four lanes of an aligned 4-pixel group (lx & 3 == gx & 3, tiles
+    // start at multiples of 16) combine their cnt bytes into one word add (no carry: cnt < 256).
+    auto project = [&](uint8_t fin) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        bool pj = g.proj && own && checked_row && fin == kAccepted && pj_sh >= 0;
+        if (pj) pj = ((S.pjm[tid] >> pj_sh) & 0xffu) != 0;
+        const int64_t ai = (int64_t)(gy - g.buf_y0) * g.acc_pitch + gx;
+        if (pj) atomicAdd(g.sum + ai, (S.pjv[tid] >> pj_sh) & 0xffu);
+        unsigned inc = pj ? 1u << (8 * (gx & 3)) : 0u;
+        inc |= __shfl_xor_sync(0xffffffffu, inc, 1);
+        inc |= __shfl_xor_sync(0xffffffffu, inc, 2);
+        if ((gx & 3) == 0 && inc) atomicAdd(reinterpret_cast<unsigned *>(g.cnt + ai), inc);
+    };
     if (own) {
         const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f_p[zr].pitch + gx;
         const bool has = st >= kCandidate;
@@ -194,7 +225,10 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
         else reinterpret_cast<uint32_t *>(g.f_p[zr].err)[fi] = has ? eu : 0u;
         if (!FRMC) g.f_p[zr].status[fi] = st;
     }
-    if (!FRMC) return;
+    if (!FRMC) {
+        project(st);
+        return;
+    }
 
     // 4. FRMC on the checkable entries (NNC survivors in the cascade): items (entry, delta_y).
     //    Supports n'(delta) of entries whose reference window lies in the frame are the measured
@@ -238,6 +272,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const EpiArgs g) {
         const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f_p[zr].pitch + gx;
         g.f_p[zr].status[fi] = checked ? (S.rej[tid] ? kRejected : kAccepted) : st;
     }
+    project(checked_row && (st == kCandidate || st == kAccepted) ? (S.rej[tid] ? kRejected : kAccepted) : st);
     if (g.evals && tid == 0 && ne) atomicAdd(g.evals, 49ull * (unsigned long long)ne);
 }
 

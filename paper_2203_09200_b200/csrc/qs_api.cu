@@ -437,13 +437,25 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
 
 int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, int32_t n_refs,
                       const void *const *refs, int64_t ref_pitch, const qs_roi *roi, const qs_me_params *p,
-                      const qs_checks *fuse, qs_field *outs, unsigned long long *eval_count, void *workspace,
-                      size_t workspace_bytes, void *stream) {
+                      const qs_checks *fuse, qs_field *outs, const qs_projection *proj,
+                      unsigned long long *eval_count, void *workspace, size_t workspace_bytes, void *stream) {
     Roi r;
     int rc;
     if (n_refs < 0) return fail(QS_EINVAL, "n_refs=%d", n_refs);
     if (n_refs > 0 && (!refs || !outs)) return fail(QS_EINVAL, "refs / outs is NULL");
     if ((rc = check_roi(roi, &r)) || (rc = check_params(p))) return rc;
+    if (proj && n_refs > 0) {
+        if (!proj->past_val || !proj->past_mask || !proj->sum || !proj->cnt)
+            return fail(QS_EINVAL, "projection: past_val / past_mask / sum / cnt is NULL");
+        if (proj->acc_pitch < r.W) return fail(QS_EDIM, "projection: acc_pitch < width");
+        if ((reinterpret_cast<uintptr_t>(proj->sum) & 3) || (reinterpret_cast<uintptr_t>(proj->cnt) & 3) ||
+            (proj->acc_pitch & 3))
+            return fail(QS_EALIGN, "projection: sum / cnt must be 4-byte aligned and acc_pitch a multiple of 4");
+        for (int i = 0; i < n_refs; ++i)
+            if ((rc = check_plane(proj->past_val[i], proj->past_pitch, r.W, "past_val")) ||
+                (rc = check_plane(proj->past_mask[i], proj->past_pitch, r.W, "past_mask")))
+                return rc;
+    }
     size_t slot = 0;
     if ((rc = qs_workspace_size(roi, r.W, r.H, p, &slot))) return rc;
     if (n_refs == 0) return QS_OK;
@@ -455,10 +467,14 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
     const bool paper = frmc && is_paper_offsets(fuse->offsets, fuse->n_offsets);
     // The single-launch path covers the fused K = 8 epilogue; everything else runs slot by slot.
     if (p->K_h != 8 || (frmc && !paper)) {
-        for (int i = 0; i < n_refs; ++i)
+        for (int i = 0; i < n_refs; ++i) {
             if ((rc = qs_me_search(cur, cur_mask, cur_pitch, refs[i], ref_pitch, roi, p, fuse, &outs[i], eval_count,
                                    ws + slot * i, slot, stream)))
                 return rc;
+            if (proj && (rc = qs_project(&outs[i], proj->past_val[i], proj->past_mask[i], proj->past_pitch, roi,
+                                         proj->sum, proj->cnt, proj->acc_pitch, stream)))
+                return rc;
+        }
         return QS_OK;
     }
     for (int i0 = 0; i0 < n_refs; i0 += kMaxRefs) {   // groups of kMaxRefs slots per launch
@@ -536,6 +552,17 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
             g.ref_p[i] = a.ref_p[i];
             g.keys_p[i] = a.keys_p[i];
             g.f_p[i] = view(&outs[i0 + i]);
+        }
+        if (proj) {
+            g.proj = 1;
+            for (int i = 0; i < n; ++i) {
+                g.pv_p[i] = proj->past_val[i0 + i];
+                g.pm_p[i] = proj->past_mask[i0 + i];
+            }
+            g.past_pitch = proj->past_pitch;
+            g.sum = proj->sum;
+            g.cnt = proj->cnt;
+            g.acc_pitch = proj->acc_pitch;
         }
         {
             ProfScope ps(P_EPILOGUE, s);

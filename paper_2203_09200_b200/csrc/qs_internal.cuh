@@ -126,6 +126,14 @@ struct EpiArgs {
     const uint8_t *ref_p[kMaxRefs];
     const unsigned long long *keys_p[kMaxRefs];
     FieldView f_p[kMaxRefs];
+    // Fused projection PR (qs_me_search_refs with a qs_projection): ACCEPTED entries of slot z add
+    // past_val(p + v) of slot z's past frame into sum / cnt (integer atomics: order-free, exact).
+    int proj;
+    const uint8_t *pv_p[kMaxRefs], *pm_p[kMaxRefs];
+    int64_t past_pitch;
+    uint32_t *sum;
+    uint8_t *cnt;                    // 4-byte aligned, acc_pitch % 4 == 0 (byte adds on the word)
+    int64_t acc_pitch;
 };
 cudaError_t launch_epilogue(const EpiArgs &g, cudaStream_t s);
 

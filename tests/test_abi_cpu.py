@@ -96,9 +96,10 @@ def test_me_search_refs_validates(lib):
     refs = (C.c_void_p * 3)(FAKE, FAKE, FAKE)
     outs = (qs.qs_field * 3)(_field(), _field(), _field())
 
-    def call(n, wsb, cur=FAKE, r=refs):
+    def call(n, wsb, cur=FAKE, r=refs, proj=None):
         return lib.qs_me_search_refs(C.c_void_p(cur), C.c_void_p(cur), 64, n, C.cast(r, C.c_void_p), 64,
-                                     C.byref(roi), C.byref(prm), None, C.cast(outs, C.c_void_p), None,
+                                     C.byref(roi), C.byref(prm), None, C.cast(outs, C.c_void_p),
+                                     C.byref(proj) if proj is not None else None, None,
                                      C.c_void_p(FAKE), wsb, None)
     assert call(-1, 3 * slot) == qs.QS_EINVAL
     assert call(0, 0) == qs.QS_OK                        # no references: nothing to do
@@ -107,3 +108,15 @@ def test_me_search_refs_validates(lib):
     assert call(3, 3 * slot, cur=FAKE + 4) == qs.QS_EALIGN
     bad = (C.c_void_p * 3)(FAKE, FAKE + 8, FAKE)
     assert call(3, 3 * slot, r=bad) == qs.QS_EALIGN      # every reference plane is checked
+    pv = (C.c_void_p * 3)(FAKE, FAKE, FAKE)
+    pj = qs.qs_projection(C.cast(pv, C.c_void_p), C.cast(pv, C.c_void_p), 64, FAKE, FAKE, 64)
+    pj_null = qs.qs_projection(C.cast(pv, C.c_void_p), C.cast(pv, C.c_void_p), 64, None, FAKE, 64)
+    assert call(3, 3 * slot, proj=pj_null) == qs.QS_EINVAL          # sum is NULL
+    pj_pitch = qs.qs_projection(C.cast(pv, C.c_void_p), C.cast(pv, C.c_void_p), 64, FAKE, FAKE, 66)
+    assert call(3, 3 * slot, proj=pj_pitch) == qs.QS_EALIGN         # cnt words: acc_pitch % 4
+    pj_cnt = qs.qs_projection(C.cast(pv, C.c_void_p), C.cast(pv, C.c_void_p), 64, FAKE, FAKE + 1, 64)
+    assert call(3, 3 * slot, proj=pj_cnt) == qs.QS_EALIGN
+    pv_bad = (C.c_void_p * 3)(FAKE, FAKE, FAKE + 4)
+    pj_pv = qs.qs_projection(C.cast(pv_bad, C.c_void_p), C.cast(pv, C.c_void_p), 64, FAKE, FAKE, 64)
+    assert call(3, 3 * slot, proj=pj_pv) == qs.QS_EALIGN            # every past plane is checked
+    assert pj is not None

@@ -441,3 +441,37 @@ def test_me_search_refs_groups_and_fallback():
     H, W = inps[0]["cur"].shape
     cur = qs.to_plane(inps[0]["cur"], DEV_)
     qs.qs_me_search_refs(cur, cur, [], qs.make_roi(W, H), qs.make_params(K=8, S=8), [])
+
+
+def test_me_search_refs_fused_projection_bit_exact():
+    # ME + NNC -> FRMC + PR of a frame's three references in one call vs the oracle's chain; then the
+    # slot-by-slot path (K = 9, no checks -> no ACCEPTED entries) leaves the accumulators untouched.
+    seq = synth.make_sequence(2)
+    t = 7
+    inps = [synth.pair_inputs(seq, t, d) for d in (1, 2, 3)]
+    H, W = inps[0]["cur"].shape
+    cur = qs.to_plane(inps[0]["cur"], DEV_)
+    msk = qs.to_plane(inps[0]["cur_mask"], DEV_)
+    refs = [qs.to_plane(i["ref"], DEV_) for i in inps]
+    pvs = [qs.to_plane(i["past_val"], DEV_) for i in inps]
+    pms = [qs.to_plane(i["past_mask"], DEV_) for i in inps]
+    roi = qs.make_roi(W, H)
+    outs = [qs.Field.alloc(H, W, False, DEV_) for _ in inps]
+    s, c = qs.alloc_acc(H, W, DEV_)
+    qs.qs_me_search_refs(cur, msk, refs, roi, qs.make_params(K=8, S=16), outs, fuse=qs.make_checks(),
+                         project=(pvs, pms, s, c))
+    torch.cuda.synchronize()
+    osum = np.zeros((H, W), np.uint32)
+    ocnt = np.zeros((H, W), np.uint8)
+    for o_f, inp in zip(outs, inps):
+        o, _ = oracle.pair_chain(inp, K=8, S=16, check="nnc_frmc")
+        g = o_f.numpy()
+        g["err"] = g["err"].view(np.uint32)
+        assert_field_equal(g, o, what="refs+PR")
+        osum, ocnt = oracle.project(o, inp["past_val"], inp["past_mask"], osum, ocnt)
+    assert int(ocnt.sum()) > 0
+    assert np.array_equal(s.cpu().numpy().view(np.uint32), osum) and np.array_equal(c.cpu().numpy(), ocnt)
+    s0, c0 = s.clone(), c.clone()
+    qs.qs_me_search_refs(cur, msk, refs[:2], roi, qs.make_params(K=9, S=4), outs[:2], project=(pvs[:2], pms[:2], s, c))
+    torch.cuda.synchronize()
+    assert torch.equal(s, s0) and torch.equal(c, c0)

@@ -66,6 +66,7 @@ def lib():
         _lib.or_rmc.argtypes = [P, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, i32]
         _lib.or_rme.argtypes = [P, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]
         _lib.or_nnc.argtypes = [i32, i32, i32, i32, vp, vp, vp, i32]
+        _lib.or_nnc_mode.argtypes = [i32, i32, i32, i32, vp, vp, vp, i32, i32]
         _lib.or_median_field.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp]
         _lib.or_project.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
         _lib.or_probe_fwd.argtypes = [P, vp, vp, vp, i32, i32, i32, i32, vp, vp, vp]
@@ -162,13 +163,16 @@ def rme(cur, cur_mask, ref, field, K=8, S=8, min_support=8, ssd=False, ref_mode=
                        rows, [], [])
 
 
-def nnc(field, threshold=1, rows=None):
-    """NNC (Eq. 1). Returns the new status plane."""
+def nnc(field, threshold=1, rows=None, pairs=False):
+    """NNC (Eq. 1). Returns the new status plane.
+
+    pairs=False: filtered centre vs each valid 4-neighbour (R15, the headline reading).
+    pairs=True: the valid 4-neighbours compared with each other (R30)."""
     st = _c(field["status"], np.uint8).copy()
     H, W = st.shape
     y0, y1 = rows if rows is not None else (0, H)
-    r = lib().or_nnc(W, H, y0, y1, _p(_c(field["alpha"], np.int8)), _p(_c(field["beta"], np.int8)), _p(st),
-                     threshold)
+    r = lib().or_nnc_mode(W, H, y0, y1, _p(_c(field["alpha"], np.int8)), _p(_c(field["beta"], np.int8)), _p(st),
+                          threshold, 1 if pairs else 0)
     if r != 0:
         raise ValueError(f"or_nnc failed: {r}")
     return st

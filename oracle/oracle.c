@@ -371,9 +371,13 @@ static int cmp_int(const void *x, const void *y) {
     return (a > b) - (a < b);
 }
 
-int or_nnc(int32_t W, int32_t H, int32_t y_begin, int32_t y_end, const int8_t *alpha, const int8_t *beta,
-           uint8_t *status, int32_t threshold) {
-    if (W <= 0 || H <= 0 || threshold < 0) return -1;
+/* mode 0: the reading above (R15).  mode 1: the other reading of "at most one for each neighboring */
+/* pair" (SPEC.md:369 open question; R30): the filtered vectors of the in-    */
+/* frame valid 4-neighbours are compared with EACH OTHER (every unordered pair of them, the centre    */
+/* not compared); REJECTED iff some pair differs by more than threshold, else ACCEPTED.               */
+int or_nnc_mode(int32_t W, int32_t H, int32_t y_begin, int32_t y_end, const int8_t *alpha, const int8_t *beta,
+                uint8_t *status, int32_t threshold, int32_t mode) {
+    if (W <= 0 || H <= 0 || threshold < 0 || mode < 0 || mode > 1) return -1;
     size_t N = (size_t)W * H;
     int *fa = (int *)malloc(sizeof(int) * N), *fb = (int *)malloc(sizeof(int) * N);
     uint8_t *valid = (uint8_t *)malloc(N);
@@ -406,17 +410,36 @@ int or_nnc(int32_t W, int32_t H, int32_t y_begin, int32_t y_end, const int8_t *a
             size_t i = (size_t)y * W + x;
             if (!checkable(status[i])) continue;
             int reject = 0;
+            size_t nbj[4];
+            int nn = 0;
             for (int k = 0; k < 4; ++k) {
                 int yy = y + NB[k][0], xx = x + NB[k][1];
                 if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
                 size_t j = (size_t)yy * W + xx;
                 if (!valid[j]) continue;
-                if (abs(fa[i] - fa[j]) + abs(fb[i] - fb[j]) > threshold) reject = 1;
+                nbj[nn++] = j;
+            }
+            if (mode == 0) {
+                for (int k = 0; k < nn; ++k) {
+                    size_t j = nbj[k];
+                    if (abs(fa[i] - fa[j]) + abs(fb[i] - fb[j]) > threshold) reject = 1;
+                }
+            } else {
+                for (int k = 0; k < nn; ++k)
+                    for (int l = k + 1; l < nn; ++l) {
+                        size_t j = nbj[k], m = nbj[l];
+                        if (abs(fa[j] - fa[m]) + abs(fb[j] - fb[m]) > threshold) reject = 1;
+                    }
             }
             status[i] = reject ? OR_REJECTED : OR_ACCEPTED;
         }
     free(fa); free(fb); free(valid);
     return 0;
+}
+
+int or_nnc(int32_t W, int32_t H, int32_t y_begin, int32_t y_end, const int8_t *alpha, const int8_t *beta,
+           uint8_t *status, int32_t threshold) {
+    return or_nnc_mode(W, H, y_begin, y_end, alpha, beta, status, threshold, 0);
 }
 
 /* Filtered field of Eq. (1) alone (for pins); undefined entries get 0 and def=0. */

@@ -178,7 +178,7 @@ def median_field(alpha, beta, status):
     return fa, fb, valid
 
 
-def nnc(alpha, beta, status, threshold=1):
+def nnc(alpha, beta, status, threshold=1, pairs=False):
     fa, fb, valid = median_field(alpha, beta, status)
     H, W = status.shape
     st = status.copy()
@@ -186,11 +186,13 @@ def nnc(alpha, beta, status, threshold=1):
         for x in range(W):
             if st[y, x] not in (CANDIDATE, ACCEPTED):
                 continue
-            bad = False
-            for yy, xx in ((y - 1, x), (y + 1, x), (y, x - 1), (y, x + 1)):
-                if 0 <= yy < H and 0 <= xx < W and valid[yy, xx]:
-                    if abs(fa[y, x] - fa[yy, xx]) + abs(fb[y, x] - fb[yy, xx]) > threshold:
-                        bad = True
+            nbs = [(yy, xx) for yy, xx in ((y - 1, x), (y + 1, x), (y, x - 1), (y, x + 1))
+                   if 0 <= yy < H and 0 <= xx < W and valid[yy, xx]]
+            if pairs:    # R30: the neighbours among themselves
+                tests = [(p, q) for i, p in enumerate(nbs) for q in nbs[i + 1:]]
+            else:        # R15: the centre against each neighbour
+                tests = [((y, x), q) for q in nbs]
+            bad = any(abs(fa[p] - fa[q]) + abs(fb[p] - fb[q]) > threshold for p, q in tests)
             st[y, x] = REJECTED if bad else ACCEPTED
     return st
 

@@ -503,3 +503,29 @@ def test_p15_fp32_within_bound_of_fp64():
         e2, n2 = oracle.cost_fwd(inp["cur"], inp["cur_mask"], inp["ref"], y, x, int(f64["alpha"][y, x]),
                                  int(f64["beta"][y, x]), K=8, ref_mode=oracle.REF_F32_ACC64)
         assert abs(e1 / n1 - e2 / n2) <= 2e-6 * max(e2 / n2, 1e-9)
+
+
+# ---------------------------------------------------------------------------
+# P7b: the two readings of NNC's "each neighboring pair" (R15 headline, R30 NEXT-4)
+# ---------------------------------------------------------------------------
+def test_p7b_nnc_pairs_reading_golden(golden):
+    g = golden("nnc_pairs_hand.json")
+    for case in g["cases"]:
+        f = dict(alpha=_arr(case["alpha"], np.int8), beta=_arr(case["beta"], np.int8),
+                 status=_arr(case["status"], np.uint8))
+        fa, _, d = oracle.median_field(f)
+        m = d == 1
+        assert np.array_equal(fa[m], _arr(case["filtered_alpha"], np.int32)[m]), case["name"]
+        for pairs, key in ((False, "expect_centre"), (True, "expect_pairs")):
+            st = oracle.nnc(f, threshold=1, pairs=pairs)
+            assert np.array_equal(st, _arr(case[key], np.uint8)), (case["name"], key)
+            assert np.array_equal(twin.nnc(f["alpha"], f["beta"], f["status"], 1, pairs=pairs), st)
+
+
+def test_p7b_nnc_pairs_equals_centre_reading_on_the_p7_fixtures(golden):
+    # On the P7 fixtures where every filtered vector is equal the two readings agree (constant fields)
+    g = golden("nnc_hand.json")
+    for case in g["cases"][:2]:
+        f = dict(alpha=_arr(case["alpha"], np.int8), beta=_arr(case["beta"], np.int8),
+                 status=_arr(case["status"], np.uint8))
+        assert np.array_equal(oracle.nnc(f, pairs=True), oracle.nnc(f, pairs=False)), case["name"]

@@ -468,20 +468,30 @@ def run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32):
     res = {}
     t = 7
 
+    # SURVEY.md 8(f) NEXT-4 variants: NNC's second reading (R30) in the cascade, and FRMC with the
+    # {0, +-(2^k - 1)} offsets extended by +-15 (valid for S >= 15)
+    ext = (-15, -7, -3, -1, 0, 1, 3, 7, 15)
+
     def check(name, d, fr, past):
         f, ws = fields[d - 1], wss[d - 1]
         if name == "nnc_frmc":
             qs.qs_nnc(f, roi)
             qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, f)
+        elif name == "nnc_pairs_frmc":
+            qs.qs_nnc_mode(f, roi, 1, qs.QS_NNC_PAIRS)
+            qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, f)
         elif name == "frmc":
             qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, f)
+        elif name == "frmc_ext15":
+            qs.qs_frmc(fr["cur"], fr["mask"], past["ref"], roi, prm, f, offsets=ext)
         elif name == "rme":
             qs.qs_reverse_check(qs.QS_RME, fr["cur"], fr["mask"], past["ref"], roi, prm, f, ws=ws)
         else:
             qs.qs_reverse_check(qs.QS_RMC, fr["cur"], fr["mask"], past["ref"], roi, prm, f)
 
     rates = {}
-    for name in ("nnc_frmc", "frmc", "rme", "rmc"):
+    names = ("nnc_frmc", "nnc_pairs_frmc", "frmc") + (("frmc_ext15",) if S >= 15 else ()) + ("rme", "rmc")
+    for name in names:
         tot = 0.0
         acc = cand = 0
         for rep in range(2):                 # rep 0: warm-up

@@ -113,8 +113,13 @@ typedef struct {
     int64_t pitch;   /* in elements, shared by the five planes */
 } qs_field;
 
+/* NNC readings of PAPER.md:114 "at most one for each neighboring pair" (R15 / R30). */
+#define QS_NNC_CENTRE 1   /* the filtered centre against each filtered 4-neighbour (headline, R15) */
+#define QS_NNC_PAIRS 2    /* the filtered 4-neighbours against each other (R30) */
+
 /* Checks fused into qs_me_search (NULL = ME only).
- *   nnc            run NNC after ME
+ *   nnc            0 = no NNC; QS_NNC_CENTRE / QS_NNC_PAIRS = run NNC
+ *                  after ME with that reading; other values QS_EINVAL
  *   nnc_threshold  accept iff |da~| + |db~| <= threshold for every tested
  *                  neighbour (paper: "at most one" -> 1)
  *   frmc           run FRMC on the entries left checkable
@@ -266,6 +271,11 @@ int qs_frmc(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
  * In-place is safe: the filter reads a snapshot taken inside the kernel.
  * ------------------------------------------------------------------------- */
 int qs_nnc(qs_field *io, const qs_roi *roi, int32_t threshold, void *stream);
+
+/* qs_nnc with the reading chosen: mode QS_NNC_CENTRE (= qs_nnc) or QS_NNC_PAIRS (the valid in-frame
+ * filtered 4-neighbours compared with each other, every unordered pair; REJECTED iff some pair differs
+ * by more than threshold; fewer than two tested neighbours -> ACCEPTED).  Other modes QS_EINVAL. */
+int qs_nnc_mode(qs_field *io, const qs_roi *roi, int32_t threshold, int32_t mode, void *stream);
 
 /* ---------------------------------------------------------------------------
  * qs_project -- projection PR (§2.2: "If a measurement is

@@ -31,6 +31,7 @@ QS_NOT_TARGET, QS_INVALID, QS_CANDIDATE, QS_ACCEPTED, QS_REJECTED = 0, 1, 2, 3, 
 QS_SAD, QS_SSD = 0, 1
 QS_REF_U8, QS_REF_F32 = 0, 1
 QS_RME, QS_RMC = 0, 1
+QS_NNC_CENTRE, QS_NNC_PAIRS = 1, 2
 
 # PAPER.md:104 (§3.1.1): FRMC tests "only motions in the set {-7,-3,-1,0,1,3,7}".
 PAPER_FRMC_OFFSETS = (-7, -3, -1, 0, 1, 3, 7)
@@ -88,8 +89,9 @@ def lib() -> C.CDLL:
                                        vp, vp, sz, vp]
         L.qs_frmc.argtypes = [vp, vp, i64, vp, i64, P(qs_roi), P(qs_me_params), vp, i32, P(qs_field), vp, vp]
         L.qs_nnc.argtypes = [P(qs_field), P(qs_roi), i32, vp]
+        L.qs_nnc_mode.argtypes = [P(qs_field), P(qs_roi), i32, i32, vp]
         L.qs_project.argtypes = [P(qs_field), vp, vp, i64, P(qs_roi), vp, vp, i64, vp]
-        for f in ("qs_workspace_size", "qs_me_search", "qs_me_search_refs", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_project"):
+        for f in ("qs_workspace_size", "qs_me_search", "qs_me_search_refs", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_nnc_mode", "qs_project"):
             getattr(L, f).restype = C.c_int
         L.qs_profile_enable.argtypes = [i32]
         L.qs_profile_read.argtypes = [C.c_char_p, P(C.c_double), P(C.c_int64)]
@@ -189,9 +191,11 @@ def make_params(K=8, S=16, min_support=8, ssd=False, ref_f32=False) -> qs_me_par
     return qs_me_params(K, K, S, min_support, QS_SSD if ssd else QS_SAD, QS_REF_F32 if ref_f32 else QS_REF_U8)
 
 
-def make_checks(nnc=True, frmc=True, threshold=1, offsets=PAPER_FRMC_OFFSETS):
+def make_checks(nnc=True, frmc=True, threshold=1, offsets=PAPER_FRMC_OFFSETS, nnc_pairs=False):
+    """nnc_pairs: NNC's second reading (QS_NNC_PAIRS, R30) instead of the headline centre reading."""
     arr = (C.c_int8 * len(offsets))(*offsets)
-    chk = qs_checks(int(nnc), threshold, int(frmc), C.cast(arr, C.c_void_p), len(offsets))
+    mode = (QS_NNC_PAIRS if nnc_pairs else QS_NNC_CENTRE) if nnc else 0
+    chk = qs_checks(mode, threshold, int(frmc), C.cast(arr, C.c_void_p), len(offsets))
     chk._keep = arr
     return chk
 
@@ -310,6 +314,11 @@ def qs_frmc(cur, cur_mask, ref, roi: qs_roi, params: qs_me_params, io: Field, of
 def qs_nnc(io: Field, roi: qs_roi, threshold: int = 1, stream=None):
     fc = io.c()
     _check(lib().qs_nnc(C.byref(fc), C.byref(roi), threshold, _stream(stream)))
+
+
+def qs_nnc_mode(io: Field, roi: qs_roi, threshold: int = 1, mode: int = QS_NNC_CENTRE, stream=None):
+    fc = io.c()
+    _check(lib().qs_nnc_mode(C.byref(fc), C.byref(roi), threshold, mode, _stream(stream)))
 
 
 def qs_project(f: Field, past_val, past_mask, roi: qs_roi, sum_: torch.Tensor, cnt: torch.Tensor, stream=None):

@@ -39,7 +39,7 @@ __device__ __forceinline__ int lower_median9(int (&v)[9], int n) {
 }
 
 __global__ void __launch_bounds__(kNX * kNY) nnc_kernel(FieldView f, int W, int H, int buf_y0, int buf_rows,
-                                                          int y0, int y1, int threshold) {
+                                                          int y0, int y1, int threshold, int mode) {
     __shared__ int sa[kNY + 4][kNX + 4], sb[kNY + 4][kNX + 4];
     __shared__ uint8_t sv[kNY + 4][kNX + 4];
     __shared__ int fa[kNY + 2][kNX + 2], fb[kNY + 2][kNX + 2];
@@ -89,17 +89,17 @@ __global__ void __launch_bounds__(kNX * kNY) nnc_kernel(FieldView f, int W, int 
     const int64_t fi = (int64_t)(gy - buf_y0) * f.pitch + gx;
     const uint8_t st = f.status[fi];
     if (!checkable(st)) return;
-    const int ca = fa[r - 1][c - 1], cb = fb[r - 1][c - 1];
-    bool reject = false;
     const int NBR[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+    int na[4], nb[4];
+    bool nv[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int rr = r + NBR[k][0], cc = c + NBR[k][1];
-        if (!sv[rr][cc]) continue;   // out of frame or not valid: skipped (R15)
-        const int d = abs(ca - fa[rr - 1][cc - 1]) + abs(cb - fb[rr - 1][cc - 1]);
-        if (d > threshold) reject = true;
+        nv[k] = sv[rr][cc];          // out of frame or not valid: skipped (R15)
+        na[k] = fa[rr - 1][cc - 1];
+        nb[k] = fb[rr - 1][cc - 1];
     }
-    f.status[fi] = reject ? kRejected : kAccepted;
+    f.status[fi] = nnc_rejects(mode, fa[r - 1][c - 1], fb[r - 1][c - 1], na, nb, nv, threshold) ? kRejected : kAccepted;
 }
 
 // ---------------------------------------------------------------------------
@@ -362,11 +362,11 @@ __global__ void project_kernel(ProjectArgs a) {
 
 }  // namespace
 
-cudaError_t launch_nnc(FieldView f, int W, int H, int buf_y0, int buf_rows, int y0, int y1, int threshold,
+cudaError_t launch_nnc(FieldView f, int W, int H, int buf_y0, int buf_rows, int y0, int y1, int threshold, int mode,
                        cudaStream_t s) {
     if (y1 <= y0) return cudaSuccess;
     dim3 blk(kNX, kNY), grd((W + kNX - 1) / kNX, (y1 - y0 + kNY - 1) / kNY);
-    nnc_kernel<<<grd, blk, 0, s>>>(f, W, H, buf_y0, buf_rows, y0, y1, threshold);
+    nnc_kernel<<<grd, blk, 0, s>>>(f, W, H, buf_y0, buf_rows, y0, y1, threshold, mode);
     return cudaGetLastError();
 }
 

@@ -181,16 +181,18 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
         if (!F32) eu = (uint32_t)ef;                 // integer-valued and < 2^24: exact
         if (NNC && checked_row) {
             const int r = ly + 2, c = lx + 2;
-            const int ca = S.fa[r - 1][c - 1], cb = S.fb[r - 1][c - 1];
-            bool reject = false;
             const int NB[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+            int na[4], nb[4];
+            bool nv[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int rr = r + NB[k][0], cc = c + NB[k][1];
-                if (!S.sv[rr][cc]) continue;
-                if (abs(ca - S.fa[rr - 1][cc - 1]) + abs(cb - S.fb[rr - 1][cc - 1]) > g.nnc_threshold) reject = true;
+                nv[k] = S.sv[rr][cc];
+                na[k] = S.fa[rr - 1][cc - 1];
+                nb[k] = S.fb[rr - 1][cc - 1];
             }
-            st = reject ? kRejected : kAccepted;
+            st = nnc_rejects(g.nnc, S.fa[r - 1][c - 1], S.fb[r - 1][c - 1], na, nb, nv, g.nnc_threshold) ? kRejected
+                                                                                                      : kAccepted;
         }
     }
     if (FRMC) {

@@ -318,6 +318,7 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
         return rc;
     const bool nnc = fuse && fuse->nnc, frmc = fuse && fuse->frmc;
     if (fuse && nnc && fuse->nnc_threshold < 0) return fail(QS_EINVAL, "nnc_threshold < 0");
+    if (fuse && (fuse->nnc < 0 || fuse->nnc > QS_NNC_PAIRS)) return fail(QS_EINVAL, "nnc mode %d", fuse->nnc);
     if (frmc && (rc = check_offsets(fuse->offsets, fuse->n_offsets, p->S))) return rc;
     const int lo = nnc ? std::max(0, r.y0 - 2) : r.y0, hi = nnc ? std::min(r.H, r.y1 + 2) : r.y1;
     const int K = p->K_h, KL = K / 2, KR = K - 1 - KL;
@@ -373,7 +374,7 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
         g.key_pitch = r.W;
         g.canon = t->canon;
         g.f = view(out);
-        g.nnc = nnc;
+        g.nnc = nnc ? fuse->nnc : 0;
         g.nnc_threshold = nnc ? fuse->nnc_threshold : 0;
         g.frmc = paper;
         const int8_t order[7] = {0, -1, 1, -3, 3, -7, 7};   // the paper's set; small offsets first
@@ -423,7 +424,7 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     if (nnc) {
         {
             ProfScope ps(P_NNC, s);
-            e = launch_nnc(view(out), r.W, r.H, r.b0, r.br, r.y0, r.y1, fuse->nnc_threshold, s);
+            e = launch_nnc(view(out), r.W, r.H, r.b0, r.br, r.y0, r.y1, fuse->nnc_threshold, fuse->nnc, s);
         }
         if (e != cudaSuccess) return cuda_fail(e, "nnc launch");
     }
@@ -487,6 +488,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
                 (rc = check_field(&outs[i0 + i], r.W, true)))
                 return rc;
         if (nnc && fuse->nnc_threshold < 0) return fail(QS_EINVAL, "nnc_threshold < 0");
+        if (fuse && (fuse->nnc < 0 || fuse->nnc > QS_NNC_PAIRS)) return fail(QS_EINVAL, "nnc mode %d", fuse->nnc);
         if (frmc && (rc = check_offsets(fuse->offsets, fuse->n_offsets, p->S))) return rc;
         const int lo = nnc ? std::max(0, r.y0 - 2) : r.y0, hi = nnc ? std::min(r.H, r.y1 + 2) : r.y1;
         const int KL = 4, KR = 3;
@@ -541,7 +543,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
         g.key_pitch = r.W;
         g.canon = t->canon;
         g.f = view(&outs[i0]);
-        g.nnc = nnc;
+        g.nnc = nnc ? fuse->nnc : 0;
         g.nnc_threshold = nnc ? fuse->nnc_threshold : 0;
         g.frmc = paper;
         const int8_t order[7] = {0, -1, 1, -3, 3, -7, 7};
@@ -659,6 +661,11 @@ int qs_frmc(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch, cons
 }
 
 int qs_nnc(qs_field *io, const qs_roi *roi, int32_t threshold, void *stream) {
+    return qs_nnc_mode(io, roi, threshold, QS_NNC_CENTRE, stream);
+}
+
+int qs_nnc_mode(qs_field *io, const qs_roi *roi, int32_t threshold, int32_t mode, void *stream) {
+    if (mode != QS_NNC_CENTRE && mode != QS_NNC_PAIRS) return fail(QS_EINVAL, "nnc mode %d", mode);
     Roi r;
     int rc;
     if ((rc = check_roi(roi, &r))) return rc;
@@ -669,7 +676,7 @@ int qs_nnc(qs_field *io, const qs_roi *roi, int32_t threshold, void *stream) {
     cudaError_t e;
     {
         ProfScope ps(P_NNC, s);
-        e = launch_nnc(view(io), r.W, r.H, r.b0, r.br, r.y0, r.y1, threshold, s);
+        e = launch_nnc(view(io), r.W, r.H, r.b0, r.br, r.y0, r.y1, threshold, mode, s);
     }
     return e == cudaSuccess ? QS_OK : cuda_fail(e, "nnc launch");
 }

@@ -105,7 +105,26 @@ struct FieldView {
     int64_t pitch;                   // elements; row 0 == global buf_y0
 };
 
-cudaError_t launch_nnc(FieldView f, int W, int H, int buf_y0, int buf_rows, int y0, int y1, int threshold,
+// NNC decision of one entry from the filtered centre (ca, cb) and its four filtered 4-neighbours
+// (nv: in frame and valid).  mode 1 (R15): the centre against each neighbour; mode 2 (R30, the other
+// reading of PAPER.md:114's "each neighboring pair"): the neighbours against each other.
+__device__ __forceinline__ bool nnc_rejects(int mode, int ca, int cb, const int (&na)[4], const int (&nb)[4],
+                                            const bool (&nv)[4], int threshold) {
+    bool reject = false;
+    if (mode == 2) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int l = k + 1; l < 4; ++l)
+                if (nv[k] && nv[l] && abs(na[k] - na[l]) + abs(nb[k] - nb[l]) > threshold) reject = true;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (nv[k] && abs(ca - na[k]) + abs(cb - nb[k]) > threshold) reject = true;
+    }
+    return reject;
+}
+cudaError_t launch_nnc(FieldView f, int W, int H, int buf_y0, int buf_rows, int y0, int y1, int threshold, int mode,
                        cudaStream_t s);
 
 // Fused per-pair epilogue for K = 8 (epilogue.cu): finalize + NNC + FRMC (paper offsets).

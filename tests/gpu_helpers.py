@@ -67,6 +67,8 @@ def gpu_check(kind, inp, field, K=8, S=8, min_support=8, ssd=False, offsets=qs.P
     ev = torch.zeros(1, dtype=torch.int64, device=dev)
     if kind == "nnc":
         qs.qs_nnc(f, roi, threshold)
+    elif kind == "nnc_pairs":
+        qs.qs_nnc_mode(f, roi, threshold, qs.QS_NNC_PAIRS)
     elif kind == "frmc":
         qs.qs_frmc(p["cur"], p["cur_mask"], p["ref"], roi, prm, f, offsets=offsets, eval_count=ev)
     elif kind == "rmc":

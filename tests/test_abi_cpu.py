@@ -21,7 +21,7 @@ def lib():
 
 def test_exports_every_header_symbol(lib):
     names = qs.header_functions()
-    assert set(names) >= {"qs_me_search", "qs_me_search_refs", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_project",
+    assert set(names) >= {"qs_me_search", "qs_me_search_refs", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_nnc_mode", "qs_project",
                           "qs_last_error", "qs_workspace_size", "qs_version"}
     for n in names:
         assert hasattr(lib, n), n
@@ -120,3 +120,14 @@ def test_me_search_refs_validates(lib):
     pj_pv = qs.qs_projection(C.cast(pv_bad, C.c_void_p), C.cast(pv, C.c_void_p), 64, FAKE, FAKE, 64)
     assert call(3, 3 * slot, proj=pj_pv) == qs.QS_EALIGN            # every past plane is checked
     assert pj is not None
+
+
+def test_nnc_mode_validates(lib):
+    roi = qs.make_roi(64, 64)
+    f = _field()
+    assert lib.qs_nnc_mode(C.byref(f), C.byref(roi), 1, 3, None) == qs.QS_EINVAL
+    assert lib.qs_nnc_mode(C.byref(f), C.byref(roi), 1, 0, None) == qs.QS_EINVAL
+    chk = qs.make_checks()
+    chk.nnc = 5
+    assert _call_me(lib, roi, qs.make_params(K=8, S=8), fuse=chk) == qs.QS_EINVAL
+    assert "nnc mode" in qs.qs_last_error()

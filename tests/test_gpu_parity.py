@@ -475,3 +475,44 @@ def test_me_search_refs_fused_projection_bit_exact():
     qs.qs_me_search_refs(cur, msk, refs[:2], roi, qs.make_params(K=9, S=4), outs[:2], project=(pvs[:2], pms[:2], s, c))
     torch.cuda.synchronize()
     assert torch.equal(s, s0) and torch.equal(c, c0)
+
+
+
+# ---------------------------------------------------------------------------
+# NNC's second reading (R30): standalone on the hand-worked fixtures, and fused
+# into qs_me_search (NNC(pairs) -> FRMC cascade) against the oracle's chain
+# ---------------------------------------------------------------------------
+def test_nnc_pairs_golden_on_gpu(golden):
+    g = golden("nnc_pairs_hand.json")
+    for case in g["cases"]:
+        a = np.array(case["alpha"], np.int8)
+        H, W = a.shape
+        Hp, Wp = H + H % 2, W + W % 2
+        fld = {k: np.zeros((Hp, Wp), dt) for k, dt in (("alpha", np.int8), ("beta", np.int8), ("err", np.uint32),
+                                                        ("count", np.uint8), ("status", np.uint8))}
+        fld["alpha"][:H, :W] = a
+        fld["beta"][:H, :W] = np.array(case["beta"], np.int8)
+        fld["status"][:H, :W] = np.array(case["status"], np.uint8)
+        inp = dict(cur=np.zeros((Hp, Wp), np.uint8), cur_mask=np.zeros((Hp, Wp), np.uint8),
+                   ref=np.zeros((Hp, Wp), np.uint8), past_val=np.zeros((Hp, Wp), np.uint8),
+                   past_mask=np.zeros((Hp, Wp), np.uint8))
+        for kind, key in (("nnc", "expect_centre"), ("nnc_pairs", "expect_pairs")):
+            st, _ = gpu_check(kind, inp, fld)
+            assert np.array_equal(st[:H, :W], np.array(case[key], np.uint8)), (case["name"], kind)
+
+
+@pytest.mark.parametrize("cfg,S", [(2, 16), (4, 9)])
+def test_nnc_pairs_cascade_fused(cfg, S):
+    seq = synth.make_sequence(cfg, w=192 if cfg == 4 else None, h=160 if cfg == 4 else None)
+    inp = synth.pair_inputs(seq, 6, 1)
+    g, gev = gpu_me(inp, K=8, S=S, fuse=qs.make_checks(nnc_pairs=True))
+    o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=8, S=S)
+    if cfg == 4:   # float reference: decide the checks on the GPU's own field (staged parity, R23)
+        o = {k: g[k].copy() for k in g}
+        o["status"] = np.where(g["status"] >= oracle.CANDIDATE, oracle.CANDIDATE, g["status"]).astype(np.uint8)
+    o["status"] = oracle.nnc(o, 1, pairs=True)
+    o["status"], oev = oracle.frmc(inp["cur"], inp["cur_mask"], inp["ref"], o, K=8, S=S)
+    assert np.array_equal(g["status"], o["status"])
+    assert gev == oev
+    if cfg == 2:
+        assert_field_equal(g, o, what="nnc pairs cascade")

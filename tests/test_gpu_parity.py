@@ -516,3 +516,48 @@ def test_nnc_pairs_cascade_fused(cfg, S):
     assert gev == oev
     if cfg == 2:
         assert_field_equal(g, o, what="nnc pairs cascade")
+
+
+def test_me_search_refs_row_bands_with_projection():
+    """The multi-GPU step on one device: each row band runs qs_me_search_refs (three references, fused
+    PR) with buffers holding only band + halo rows; the union equals the full-frame oracle chain."""
+    seq = synth.make_sequence(2)
+    t, S, K = 9, 16, 8
+    inps = [synth.pair_inputs(seq, t, d) for d in (1, 2, 3)]
+    H, W = inps[0]["cur"].shape
+    G = 2
+    bounds = [2 * ((r * H) // (2 * G)) for r in range(G + 1)]
+    halo = S + K + 2
+    gsum = np.zeros((H, W), np.uint32)
+    gcnt = np.zeros((H, W), np.uint8)
+    fields = [{k: None for k in ("alpha", "beta", "err", "count", "status")} for _ in inps]
+    for r in range(G):
+        y0, y1 = bounds[r], bounds[r + 1]
+        b0, b1 = max(0, y0 - halo), min(H, y1 + halo)
+        br = b1 - b0
+        cur = qs.to_plane(inps[0]["cur"][b0:b1], DEV_)
+        msk = qs.to_plane(inps[0]["cur_mask"][b0:b1], DEV_)
+        refs = [qs.to_plane(i["ref"][b0:b1], DEV_) for i in inps]
+        pvs = [qs.to_plane(i["past_val"][b0:b1], DEV_) for i in inps]
+        pms = [qs.to_plane(i["past_mask"][b0:b1], DEV_) for i in inps]
+        outs = [qs.Field.alloc(br, W, False, DEV_) for _ in inps]
+        s, c = qs.alloc_acc(br, W, DEV_)
+        qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H, y0, y1, b0, br), qs.make_params(K=K, S=S), outs,
+                             fuse=qs.make_checks(), project=(pvs, pms, s, c))
+        torch.cuda.synchronize()
+        gsum[y0:y1] = s.cpu().numpy().view(np.uint32)[y0 - b0:y1 - b0]
+        gcnt[y0:y1] = c.cpu().numpy()[y0 - b0:y1 - b0]
+        for f, o in zip(fields, outs):
+            g = o.numpy()
+            g["err"] = g["err"].view(np.uint32)
+            for k in f:
+                if f[k] is None:
+                    f[k] = np.zeros((H, W), g[k].dtype)
+                f[k][y0:y1] = g[k][y0 - b0:y1 - b0]
+    osum = np.zeros((H, W), np.uint32)
+    ocnt = np.zeros((H, W), np.uint8)
+    for f, inp in zip(fields, inps):
+        o, _ = oracle.pair_chain(inp, K=K, S=S, check="nnc_frmc")
+        assert_field_equal(f, o, what="refs bands")
+        osum, ocnt = oracle.project(o, inp["past_val"], inp["past_mask"], osum, ocnt)
+    assert np.array_equal(gsum, osum) and np.array_equal(gcnt, ocnt)

@@ -273,13 +273,21 @@ __global__ void __launch_bounds__(256) revgrid_tile_kernel(const TileGridArgs g)
         const int ly = pk & 0xff, lx = (pk >> 8) & 0xff;
         const int va = (int)(int8_t)((pk >> 16) & 0xff), vb = (int)(int8_t)((pk >> 24) & 0xff);
         // PAT 1 visits delta_y = 0, -1, 1, -2, 2, ... (small offsets reject wrong vectors first)
-        const int dy = PAT == 0 ? g.dys[iy] : ((iy & 1) ? -((iy + 1) >> 1) : (iy >> 1));
-        const int dx0 = PAT == 0 ? -7 : g.lo + 7 * grp;
-        const int nk = PAT == 0 ? 7 : (grp == g.n_groups - 1 ? g.n_last : 7);
+        const int dy = PAT != 1 ? g.dys[iy] : ((iy & 1) ? -((iy + 1) >> 1) : (iy >> 1));
         const uint32_t n0 = F32 ? ent_e0[e] : (uint32_t)__float_as_int(ent_m0[e]);
-        if (tile::frmc_item<PAT, SSD, F32>(R, ty0, tx0, ly, lx, va, vb, dy, dx0, nk, a.min_support, ent_m0[e],
-                                           ent_e0[e], n0, cnt8, cw))
-            rej[e] = 1;
+        bool r;
+        if constexpr (PAT == 2) {   // the +-15 set: group 0 = {-15,-7,-3,-1,0,1,3}, group 1 = {7, 15}
+            r = grp == 0 ? tile::frmc_item<2, SSD, F32>(R, ty0, tx0, ly, lx, va, vb, dy, -15, 7, a.min_support,
+                                                        ent_m0[e], ent_e0[e], n0, cnt8, cw)
+                         : tile::frmc_item<3, SSD, F32>(R, ty0, tx0, ly, lx, va, vb, dy, 7, 2, a.min_support,
+                                                        ent_m0[e], ent_e0[e], n0, cnt8, cw);
+        } else {
+            const int dx0 = PAT == 0 ? -7 : g.lo + 7 * grp;
+            const int nk = PAT == 0 ? 7 : (grp == g.n_groups - 1 ? g.n_last : 7);
+            r = tile::frmc_item<PAT, SSD, F32>(R, ty0, tx0, ly, lx, va, vb, dy, dx0, nk, a.min_support, ent_m0[e],
+                                               ent_e0[e], n0, cnt8, cw);
+        }
+        if (r) rej[e] = 1;
     }
     __syncthreads();
     for (int e = tid; e < ne; e += blockDim.x) {
@@ -386,6 +394,29 @@ cudaError_t launch_revgrid(const RevGridArgs &a, cudaStream_t s) {
             paper = seen == 0x7f;
         }
         const int S = a.full_hi;
+        // The paper's set extended by +-15: {0, +-1, +-3, +-7, +-15}.
+        bool ext15 = false;
+        if (a.n_dy == 9) {
+            int seen = 0;
+            for (int i = 0; i < 9; ++i) {
+                const int o = a.dys_host[i];
+                const int idx = o == -15 ? 0 : o == -7 ? 1 : o == -3 ? 2 : o == -1 ? 3 : o == 0 ? 4 : o == 1 ? 5
+                              : o == 3 ? 6 : o == 7 ? 7 : o == 15 ? 8 : -1;
+                if (idx >= 0) seen |= 1 << idx;
+            }
+            ext15 = seen == 0x1ff;
+        }
+        if (ext15) {
+            g.n_dy = 9;
+            const int8_t order[9] = {0, -1, 1, -3, 3, -7, 7, -15, 15};   // small offsets first
+            for (int i = 0; i < 9; ++i) g.dys[i] = order[i];
+            g.n_groups = 2;
+            g.n_last = 2;
+            g.maxd = 15;
+            g.S = S;
+            g.n_total = 81;
+            return launch_tile_p<2>(g, s);
+        }
         if (paper) {
             g.n_dy = 7;
             const int8_t order[7] = {0, -1, 1, -3, 3, -7, 7};   // the same set; small offsets first

@@ -21,11 +21,21 @@ constexpr int kFT = 16;          // tile edge (entries)
 constexpr int kFK = 8;           // template
 constexpr int kFSeg = kFK + 14;  // current-row segment per FRMC item (22)
 
-// Column of delta_x within a 15-wide group span (delta_x - dx0).
-// PAT 0 = the paper's {-7,-3,-1,0,1,3,7}; PAT 1 = 7 consecutive values.
+// Column of delta_x within an item's span (delta_x - dx0).
+// PAT 0 = the paper's {-7,-3,-1,0,1,3,7}; PAT 1 = 7 consecutive values;
+// PAT 2 / 3 = the two groups of the set extended by +-15:
+// {-15,-7,-3,-1,0,1,3} (dx0 = -15) and {7, 15} (dx0 = 7; k >= 2 unused).
 template <int PAT>
 __device__ __forceinline__ constexpr int pat_j(int k) {
-    return PAT == 0 ? (k == 0 ? 0 : k == 1 ? 4 : k == 2 ? 6 : k == 3 ? 7 : k == 4 ? 8 : k == 5 ? 10 : 14) : k;
+    return PAT == 0   ? (k == 0 ? 0 : k == 1 ? 4 : k == 2 ? 6 : k == 3 ? 7 : k == 4 ? 8 : k == 5 ? 10 : 14)
+           : PAT == 2 ? (k == 0 ? 0 : k == 1 ? 8 : k == 2 ? 12 : k == 3 ? 14 : k == 4 ? 15 : k == 5 ? 16 : 18)
+           : PAT == 3 ? (k == 1 ? 8 : 0)
+                      : k;
+}
+// Current-row segment of an item: the template width plus the item's delta_x span (even).
+template <int PAT>
+__device__ __forceinline__ constexpr int seg_len() {
+    return PAT == 2 ? kFK + 18 : PAT == 3 ? kFK + 8 : kFSeg;
 }
 
 // Packed fp32x2 subtraction (sm_100a FADD2) of (a0, a1) - (b0, b1), per-lane IEEE round-to-nearest.
@@ -146,6 +156,8 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
                                           int dx0, int nk, int min_support, float m0, uint32_t e0, uint32_t n0,
                                           const uint8_t *cnt8 = nullptr, int cw = 0) {
     constexpr int KL = kFK / 2;
+    constexpr int kSeg = seg_len<PAT>();
+    constexpr int kK = PAT == 3 ? 2 : 7;   // delta_x slots the pattern can hold (the rest stay settled)
     float acc[7], thr[7];
     int cnt[7];
 #pragma unroll
@@ -160,14 +172,14 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
     // 1. Supports n'(delta) (R6, R9): slots holding a term.
     if (cnt8 && colm == 0xffu && xy >= 0 && xy + kFK <= g.H) {
 #pragma unroll
-        for (int k = 0; k < 7; ++k) cnt[k] = cnt8[crow * cw + ccol + pat_j<PAT>(k)];
+        for (int k = 0; k < kK; ++k) cnt[k] = cnt8[crow * cw + ccol + pat_j<PAT>(k)];
     } else {
 #pragma unroll 1
         for (int oy = 0; oy < kFK; ++oy) {
             const uint32_t rb = (xy + oy >= 0 && xy + oy < g.H) ? colm : 0u;
             const uint32_t bits = mask_bits(g, crow + oy, ccol);
 #pragma unroll
-            for (int k = 0; k < 7; ++k) cnt[k] += __popc((bits >> pat_j<PAT>(k)) & rb);
+            for (int k = 0; k < kK; ++k) cnt[k] += __popc((bits >> pat_j<PAT>(k)) & rb);
         }
     }
     // 2. Settled deltas: out of the set, delta = 0, SENTINEL (n' < min_support never rejects, R11);
@@ -190,19 +202,19 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
         for (int oy = 0; oy < kFK && settled != 0x7fu; ++oy) {
             const float *cp = g.Cs + (crow + oy) * g.cpitch + ccol;
             const float *rp = g.Rs + (rrow + oy) * g.rpitch + rcol;
-            float c[kFSeg], r[kFK];
+            float c[kSeg], r[kFK];
 #pragma unroll
-            for (int j = 0; j < kFSeg; ++j) c[j] = cp[j];
+            for (int j = 0; j < kSeg; ++j) c[j] = cp[j];
 #pragma unroll
             for (int j = 0; j < kFK; ++j) r[j] = rp[j];
             const uint32_t bits = mask_bits(g, crow + oy, ccol);
             // Bit positions in pairs (b, b + 1): for an even offset j the two differences of a delta
             // are one aligned FADD2 (r[ox], r[ox+1]) - (c[b], c[b+1]); per delta still ascending ox.
 #pragma unroll
-            for (int b = 0; b < kFSeg; b += 2) {
+            for (int b = 0; b < kSeg; b += 2) {
                 const bool term0 = (bits >> b) & 1u, term1 = (bits >> (b + 1)) & 1u;
 #pragma unroll
-                for (int k = 0; k < 7; ++k) {
+                for (int k = 0; k < kK; ++k) {
                     const int j = pat_j<PAT>(k), ox = b - j;
                     if ((j & 1) == 0) {
                         if (ox < 0 || ox >= kFK) continue;
@@ -223,7 +235,7 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
                 }
             }
 #pragma unroll
-            for (int k = 0; k < 7; ++k)
+            for (int k = 0; k < kK; ++k)
                 if (acc[k] >= thr[k]) settled |= 1u << k;
         }
     } else {
@@ -231,15 +243,15 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
     for (int oy = 0; oy < kFK && settled != 0x7fu; ++oy) {
         const float *cp = g.Cs + (crow + oy) * g.cpitch + ccol;
         const float *rp = g.Rs + (rrow + oy) * g.rpitch + rcol;
-        float c[kFSeg], r[kFK];
+        float c[kSeg], r[kFK];
 #pragma unroll
-        for (int j = 0; j < kFSeg; ++j) c[j] = cp[j];
+        for (int j = 0; j < kSeg; ++j) c[j] = cp[j];
 #pragma unroll
         for (int j = 0; j < kFK; ++j) r[j] = rp[j];
         const uint32_t rb = (xy + oy >= 0 && xy + oy < g.H) ? colm : 0u;
         const uint32_t bits = mask_bits(g, crow + oy, ccol);
 #pragma unroll
-        for (int k = 0; k < 7; ++k) {
+        for (int k = 0; k < kK; ++k) {
             const int j = pat_j<PAT>(k);
             const uint32_t vm = (bits >> j) & rb;              // slots holding a term (R9)
             float dd[kFK];
@@ -263,7 +275,7 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
     if (settled == 0x7fu) return false;
     bool reject = false;
 #pragma unroll
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 0; k < kK; ++k) {
         if (settled & (1u << k)) continue;
         if (F32) {
             if (__fdiv_rn(acc[k], (float)cnt[k]) < m0) reject = true;

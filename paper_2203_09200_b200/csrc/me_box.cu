@@ -463,12 +463,30 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
 
     // Stage the chunk's reference window (rows py0-4+alo .., cols px0-4-S ..) and candidate list.
     const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
-    for (int i = threadIdx.x; i < nrow_b * ncol_b; i += kNT) {
-        const int r = i / ncol_b, c = i - r * ncol_b;
-        Bw[(r & 1) * bplane + (r >> 1) * bpitch + c] = load_ref(a, by0 + r, bx0 + c);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {
+        // One window row per warp iteration, lanes along the row (coalesced, no index division).
+        // float references: in-frame values go global -> shared by cp.async (no register round
+        // trip, many copies in flight); everything else (uint8 conversion, NaN outside the frame or
+        // the buffer) through registers.
+        const uint8_t *rp = a.ref_p[ref_slot(a)];
+        for (int r = warp; r < nrow_b; r += kNT / 32) {
+            const int y = by0 + r;
+            const bool row_in = y >= 0 && y < a.H && y >= a.buf_y0 && y < a.buf_y0 + a.buf_rows;
+            float *dst = Bw + (r & 1) * bplane + (r >> 1) * bpitch;
+            const float *src = reinterpret_cast<const float *>(rp + (int64_t)(y - a.buf_y0) * a.ref.pitch);
+            for (int c = lane; c < ncol_b; c += 32) {
+                const int x = bx0 + c;
+                if (a.ref_f32 && row_in && x >= 0 && x < a.W)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst + c)),
+                                 "l"(src + x));
+                else
+                    dst[c] = load_ref(a, y, x);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
     }
     const int k0g = a.chunk_off[chunk], nkc = a.chunk_off[chunk + 1] - k0g;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int nA = nkc, nB = 0;
     if constexpr (!BORDER) {
         for (int i = threadIdx.x; i < nkc; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);

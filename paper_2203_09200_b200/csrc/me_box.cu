@@ -546,12 +546,16 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             for (int kk = 0; kk < kQGI; ++kk) {
                 const int bk = kQRunI * half - 2 + kk;
                 const int y = py0 + 2 * bi, x = px0 + 2 * bk;
+                // blocks below the frame / the buffer (a band's ragged last tile): weight 0; they feed
+                // only outputs that are never merged
+                const bool inside = y + 1 < a.H && y + 1 < a.buf_y0 + a.buf_rows;
                 const int64_t r = (int64_t)(y - a.buf_y0);
                 const uint8_t *m0 = a.mask.p + r * a.mask.pitch + x;
-                const int q = m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
+                const int q = !inside ? 0 : m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
                 const int dy = q >> 1, dx = q & 1;
-                cv[kk] = (float)a.cur.p[(r + dy) * a.cur.pitch + x + dx];
-                wy2[kk] = f2pack(kKeyScale * (float)(1 - dy), kKeyScale * (float)dy);   // x 2^9 when keyed
+                cv[kk] = inside ? (float)a.cur.p[(r + dy) * a.cur.pitch + x + dx] : 0.f;
+                wy2[kk] = inside ? f2pack(kKeyScale * (float)(1 - dy), kKeyScale * (float)dy)   // x 2^9 when keyed
+                                 : f2pack(0.f, 0.f);
                 wx[kk] = (float)dx;
                 ad[kk] = 4 * (dy * bplane + (bi + 2) * bpitch + (2 * bk + dx + 4 + a.S));
             }
@@ -917,9 +921,13 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
             // Quarter-sampling body.  Interior: every pixel it touches, for every candidate, lies in the
             // frame and in the caller's buffer.  Border: clip-free candidates here, the rest below.
             if (a.S >= 4 && quad_mask_ok(a, px0, py0)) {
-                const bool geom = (py0 - 4 - a.S >= 0) && (py0 + 2 * kQHR - 5 + a.S <= a.H - 1) &&
+                // Rows: only the outputs the merge keeps (rows < oy1) must have every window in the
+                // frame and the buffer; rows beyond (a band's ragged last tile) read NaN windows and
+                // are never merged.  Columns: the whole tile (ox1 is the frame width).
+                const int ylast = min(py0 + kTY, a.oy1) - 1;
+                const bool geom = (py0 - 4 - a.S >= 0) && (ylast + 3 + a.S <= a.H - 1) &&
                                   (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1) &&
-                                  (py0 - 4 - a.S >= a.buf_y0) && (py0 + 2 * kQHR - 5 + a.S < a.buf_y0 + a.buf_rows);
+                                  (py0 - 4 - a.S >= a.buf_y0) && (ylast + 3 + a.S < a.buf_y0 + a.buf_rows);
                 if (geom) {
                     quad_body<SSD, EXACT, false>(a, smem, chunk, px0, py0);
                     return;

@@ -170,7 +170,8 @@ def run_ours(args):
         band = rowband.band_of(0, 1, H, rowband.halo_rows(S, K))
         seq, frames = make_frames(args.config, args.frames, s=rank)
     else:
-        band = rowband.band_of(rank, world, H, rowband.halo_rows(S, K))
+        # cost-balanced row bands (rowband.plan_bands: border tiles weigh 1.75 interior tiles)
+        band = rowband.band_of(rank, world, H, rowband.halo_rows(S, K), S=S, K=K)
         seq, frames = make_frames(args.config, args.frames)
     banded = world > 1 and not args.sequences
 

@@ -47,11 +47,78 @@ class Band:
         return self.b1 - self.b0
 
 
-def band_of(rank: int, world: int, H: int, h: int) -> Band:
+# me_box tiling (paper_2203_09200_b200/csrc): 56-row tiles from the first ME row (the band's first row
+# minus the 2-row NNC halo); a tile runs the slower border phases when an output it keeps has a window
+# that can leave the frame (measured on config 4: 1.75x an interior tile).
+TILE_ROWS = 56
+BORDER_TILE_COST = 1.75
+
+
+def band_cost(y0: int, y1: int, H: int, S: int, K: int = 8) -> float:
+    """Estimated me_box time of the band [y0, y1) in interior-tile units (one tile column)."""
+    lo, hi = max(0, y0 - 2), min(H, y1 + 2)
+    cost = 0.0
+    for py0 in range(lo, hi, TILE_ROWS):
+        ylast = min(py0 + TILE_ROWS, hi) - 1
+        border = py0 - K // 2 - S < 0 or ylast + (K - 1 - K // 2) + S > H - 1
+        cost += BORDER_TILE_COST if border else 1.0
+    return cost
+
+
+def plan_bands(world: int, H: int, S: int, K: int = 8, h: int | None = None) -> list[int]:
+    """Even row cuts 0 = c_0 < ... < c_world = H minimising the largest band_cost (bands at least h
+    rows): the smallest cost bound T for which greedy packing covers the frame, then the cuts."""
+    h = halo_rows(S, K) if h is None else h
+    if world == 1:
+        return [0, H]
+
+    def pack(T):
+        cuts, y0 = [0], 0
+        for r in range(world - 1):
+            rest = world - 1 - r                          # bands still to place after this one
+            y1 = y0 + h + (h & 1)
+            best = None
+            while y1 <= H - rest * (h + (h & 1)):
+                if band_cost(y0, y1, H, S, K) <= T:
+                    best = y1
+                y1 += 2
+            if best is None:
+                return None
+            cuts.append(best)
+            y0 = best
+        if H - y0 < h or band_cost(y0, H, H, S, K) > T:
+            return None
+        return cuts + [H]
+
+    def worst(cuts):
+        return max(band_cost(cuts[i], cuts[i + 1], H, S, K) for i in range(world))
+
+    # band_cost is not monotone in y0 (the tile grid starts at y0 - 2), so greedy packing is not
+    # optimal on its own: keep the best of the even split and the greedy plan.
+    even = [2 * ((r * H) // (2 * world)) for r in range(world)] + [H]
+    plans = [even] if min(even[i + 1] - even[i] for i in range(world)) >= h else []
+    t = 1.0
+    while t <= 4 * H:
+        cuts = pack(t)
+        if cuts is not None:
+            plans.append(cuts)
+            break
+        t += 0.25
+    if not plans:
+        raise ValueError("no band plan")
+    return min(plans, key=worst)
+
+
+def band_of(rank: int, world: int, H: int, h: int, S: int | None = None, K: int = 8) -> Band:
+    """Rank r's band: an even split of the rows, or (S given) the cost-balanced plan_bands split."""
     if world < 1 or not (0 <= rank < world):
         raise ValueError("bad rank/world")
-    y0 = 2 * ((rank * H) // (2 * world))
-    y1 = 2 * (((rank + 1) * H) // (2 * world)) if rank + 1 < world else H
+    if S is not None and world > 1:
+        cuts = plan_bands(world, H, S, K, h)
+        y0, y1 = cuts[rank], cuts[rank + 1]
+    else:
+        y0 = 2 * ((rank * H) // (2 * world))
+        y1 = 2 * (((rank + 1) * H) // (2 * world)) if rank + 1 < world else H
     if world > 1 and y1 - y0 < h:
         raise ValueError(f"band of {y1 - y0} rows is thinner than the halo ({h}); use fewer ranks")
     return Band(rank, world, H, h, y0, y1)

@@ -69,3 +69,26 @@ def test_halo_exchange_gloo(world, pitch):
     for p in procs:
         p.join(timeout=60)
     assert all(res[r] for r in range(world)), res
+
+
+def test_plan_bands_cover_balance_and_halo():
+    """rowband.plan_bands: even cuts covering [0, H), every band at least the halo, and a largest
+    estimated cost no worse than the even split's (SURVEY.md 8(e) row bands)."""
+    for (H, S, K) in ((1080, 24, 8), (2160, 32, 8), (720, 16, 8), (288, 16, 8), (64, 8, 8)):
+        h = rowband.halo_rows(S, K)
+        for G in (1, 2, 3, 4, 8):
+            if G > 1 and H // G < h:
+                continue
+            cuts = rowband.plan_bands(G, H, S, K)
+            assert cuts[0] == 0 and cuts[-1] == H and len(cuts) == G + 1
+            assert all(c % 2 == 0 for c in cuts)
+            assert all(cuts[i + 1] - cuts[i] >= (h if G > 1 else 1) for i in range(G))
+            worst = max(rowband.band_cost(cuts[i], cuts[i + 1], H, S, K) for i in range(G))
+            even = [2 * ((r * H) // (2 * G)) for r in range(G)] + [H]
+            if min(even[i + 1] - even[i] for i in range(G)) >= h:
+                assert worst <= max(rowband.band_cost(even[i], even[i + 1], H, S, K) for i in range(G))
+            bands = [rowband.band_of(r, G, H, h, S=S, K=K) for r in range(G)]
+            assert [b.y0 for b in bands] + [bands[-1].y1] == cuts
+    # config 4 on 8 ranks: the edge bands shrink (their tiles run the border phases)
+    cuts = rowband.plan_bands(8, 1080, 24, 8)
+    assert cuts[1] - cuts[0] < 135 and cuts[-1] - cuts[-2] < 135

@@ -52,12 +52,16 @@ class Band:
 # that can leave the frame (measured on config 4: 1.75x an interior tile).
 TILE_ROWS = 56
 BORDER_TILE_COST = 1.75
+# the fused epilogue (checks + PR) per output row, in the same unit (config 4: 0.66 ms per reference
+# and frame against 0.13 ms per interior tile row and reference)
+EPILOGUE_PER_ROW = 0.0047
 
 
 def band_cost(y0: int, y1: int, H: int, S: int, K: int = 8) -> float:
-    """Estimated me_box time of the band [y0, y1) in interior-tile units (one tile column)."""
+    """Estimated step time of the band [y0, y1) in interior-tile-row units: me_box tiles (from
+    the first ME row, border tiles weighted) plus the epilogue's rows."""
     lo, hi = max(0, y0 - 2), min(H, y1 + 2)
-    cost = 0.0
+    cost = EPILOGUE_PER_ROW * (y1 - y0)
     for py0 in range(lo, hi, TILE_ROWS):
         ylast = min(py0 + TILE_ROWS, hi) - 1
         border = py0 - K // 2 - S < 0 or ylast + (K - 1 - K // 2) + S > H - 1
@@ -97,13 +101,17 @@ def plan_bands(world: int, H: int, S: int, K: int = 8, h: int | None = None) -> 
     # optimal on its own: keep the best of the even split and the greedy plan.
     even = [2 * ((r * H) // (2 * world)) for r in range(world)] + [H]
     plans = [even] if min(even[i + 1] - even[i] for i in range(world)) >= h else []
-    t = 1.0
-    while t <= 4 * H:
-        cuts = pack(t)
+    lo_t, hi_t = 0.0, band_cost(0, H, H, S, K)          # feasibility of pack(T) is monotone in T
+    best = pack(hi_t)
+    for _ in range(40):
+        mid = 0.5 * (lo_t + hi_t)
+        cuts = pack(mid)
         if cuts is not None:
-            plans.append(cuts)
-            break
-        t += 0.25
+            best, hi_t = cuts, mid
+        else:
+            lo_t = mid
+    if best is not None:
+        plans.append(best)
     if not plans:
         raise ValueError("no band plan")
     return min(plans, key=worst)

@@ -62,7 +62,10 @@ struct RegionSizes {
         (void)KL;
         CR = kFT + 2 * maxd + kFK - 1;
         CC = CR;
-        cpitch = CC + 16 + 1;   // room for a 22-wide read past the region edge
+        // room for a 22-wide read past the region edge; pitch = 16 mod 32 words so the two
+        // half-warps of an FRMC row (lanes on consecutive region rows) read disjoint bank halves
+        cpitch = ((CC + 17 + 15) & ~31) + 16;
+        if (cpitch < CC + 17) cpitch += 32;
         mwords = (CC + 16 + 31) / 32 + 1;
         RR = kFT + 2 * S + kFK - 1;
         RC = RR;

@@ -292,7 +292,7 @@ extern "C" {
 
 const char *qs_last_error(void) { return g_err.c_str(); }
 
-const char *qs_version(void) { return "libqs 0.2 sm_100a (me_box quarter-sampling producer/consumer body + border phases, parity chunks; fused finalize-NNC-FRMC epilogue)"; }
+const char *qs_version(void) { return "libqs 0.3 sm_100a (me_box quarter-sampling producer/consumer body + border phases, parity chunks; fused finalize-NNC-FRMC-PR epilogue; multi-reference launches)"; }
 
 int qs_workspace_size(const qs_roi *roi, int32_t frame_w, int32_t frame_h, const qs_me_params *p, size_t *bytes) {
     Roi r;

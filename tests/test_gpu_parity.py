@@ -561,3 +561,29 @@ def test_me_search_refs_row_bands_with_projection():
         assert_field_equal(f, o, what="refs bands")
         osum, ocnt = oracle.project(o, inp["past_val"], inp["past_mask"], osum, ocnt)
     assert np.array_equal(gsum, osum) and np.array_equal(gcnt, ocnt)
+
+
+@pytest.mark.parametrize("cfg,ssd", [(3, False), (2, True)])
+def test_me_search_refs_fixed_mask_and_ssd(cfg, ssd):
+    """qs_me_search_refs on a fixed-mask config and with SSD (the generic phase-2 body for uint8 SSD)
+    against the oracle's chain, reference by reference."""
+    seq = synth.make_sequence(cfg, w=160, h=128)
+    inps = [synth.pair_inputs(seq, 5, d) for d in (1, 2, 3)]
+    H, W = inps[0]["cur"].shape
+    cur = qs.to_plane(inps[0]["cur"], DEV_)
+    msk = qs.to_plane(inps[0]["cur_mask"], DEV_)
+    refs = [qs.to_plane(i["ref"], DEV_) for i in inps]
+    outs = [qs.Field.alloc(H, W, False, DEV_) for _ in inps]
+    ev = torch.zeros(1, dtype=torch.int64, device=DEV_)
+    S = 9
+    qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H), qs.make_params(K=8, S=S, ssd=ssd), outs,
+                         fuse=qs.make_checks(), eval_count=ev)
+    torch.cuda.synchronize()
+    oev = 0
+    for o_f, inp in zip(outs, inps):
+        o, e = oracle.pair_chain(inp, K=8, S=S, ssd=ssd, check="nnc_frmc")
+        g = o_f.numpy()
+        g["err"] = g["err"].view(np.uint32)
+        assert_field_equal(g, o, what=f"refs cfg{cfg} ssd={ssd}")
+        oev += e
+    assert int(ev.item()) == oev

@@ -21,14 +21,16 @@ constexpr int kH1 = kFT + 2;   // filtered window: tile + 1-pixel halo
 constexpr int kCW = kFT + 14;  // FRMC window positions per axis (tile + the paper offsets' +-7)
 
 __device__ __forceinline__ int lower_median9(int (&v)[9], int n) {
+    // 25-comparator sorting network for 9 inputs (verified on all 2^9 0/1 inputs: 0-1 principle)
+    constexpr int kNet[25][2] = {{0, 1}, {3, 4}, {6, 7}, {1, 2}, {4, 5}, {7, 8}, {0, 1}, {3, 4}, {6, 7},
+                                 {0, 3}, {3, 6}, {0, 3}, {1, 4}, {4, 7}, {1, 4}, {2, 5}, {5, 8}, {2, 5},
+                                 {1, 3}, {5, 7}, {2, 6}, {4, 6}, {2, 4}, {2, 3}, {5, 6}};
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8 - i; ++j) {
-            const int a = v[j], b = v[j + 1];
-            v[j] = min(a, b);
-            v[j + 1] = max(a, b);
-        }
+    for (int c = 0; c < 25; ++c) {
+        const int a = v[kNet[c][0]], b = v[kNet[c][1]];
+        v[kNet[c][0]] = min(a, b);
+        v[kNet[c][1]] = max(a, b);
+    }
     int r = v[0];
 #pragma unroll
     for (int i = 1; i < 9; ++i)

@@ -188,8 +188,9 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
  * of qs_me_search(cur, cur_mask, cur_pitch, refs[i], ref_pitch, roi, p, fuse,
  * &outs[i], ...), with ME and the fused checks of all references in ONE launch
  * per kernel (K = 8 with the paper's FRMC offsets or no FRMC; other settings run
- * the calls one by one).  The template statics of the current frame are shared
- * by the references' CTAs, which run side by side (no per-reference tail).
+ * the calls one by one).  The CTAs of the references for one tile and chunk run
+ * side by side (the current frame's tile is read from L2 by all of them; no
+ * per-reference tail between launches).
  *
  *   refs        HOST array of n_refs DEVICE reference planes (same type, pitch)
  *   outs        HOST array of n_refs fields (each with its own planes / pitch)
@@ -197,7 +198,8 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
  *               ACCEPTED entries project past_val[i] / past_mask[i] into sum / cnt
  *               exactly as qs_project(&outs[i], past_val[i], past_mask[i], ...) for
  *               i = 0..n_refs-1 would (integer sums: the result does not depend on
- *               the order).  cnt must be 4-byte aligned with acc_pitch % 4 == 0, and
+ *               the order); the past planes hold the rows qs_project needs.  cnt must be
+ *               4-byte aligned with acc_pitch % 4 == 0, and
  *               every cnt byte must stay < 256 (it does for <= 255 references on a
  *               zeroed plane).
  *   eval_count  nullable device counter: the sum over the references

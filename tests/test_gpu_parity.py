@@ -587,3 +587,45 @@ def test_me_search_refs_fixed_mask_and_ssd(cfg, ssd):
         assert_field_equal(g, o, what=f"refs cfg{cfg} ssd={ssd}")
         oev += e
     assert int(ev.item()) == oev
+
+
+def test_fullsize_config4_bench_launch_sampled():
+    """The launch bench.py times: config 4 at full size, qs_me_search_refs over d = 1..3 with the fused
+    NNC -> FRMC cascade and fused PR.  Sampled rows (frame edges + interior): ME within the float
+    tolerance (f32_me_compare), then the checks and PR of the oracle run on the GPU's own vectors
+    (staged parity, R23) must give the same statuses and the same sum / cnt."""
+    c = synth.CONFIGS[4]
+    seq = synth.make_sequence(4)
+    t = 4
+    inps = [synth.pair_inputs(seq, t, d) for d in (1, 2, 3)]
+    H, W = c.h, c.w
+    cur = qs.to_plane(inps[0]["cur"], DEV_)
+    msk = qs.to_plane(inps[0]["cur_mask"], DEV_)
+    refs = [qs.to_plane(i["ref"], DEV_) for i in inps]
+    pvs = [qs.to_plane(i["past_val"], DEV_) for i in inps]
+    pms = [qs.to_plane(i["past_mask"], DEV_) for i in inps]
+    outs = [qs.Field.alloc(H, W, True, DEV_) for _ in inps]
+    s, cn = qs.alloc_acc(H, W, DEV_)
+    qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H), qs.make_params(K=8, S=c.S, ref_f32=True), outs,
+                         fuse=qs.make_checks(), project=(pvs, pms, s, cn))
+    torch.cuda.synchronize()
+    gsum, gcnt = s.cpu().numpy().view(np.uint32), cn.cpu().numpy()
+    gf = [o.numpy() for o in outs]
+    rng = np.random.default_rng(44)
+    for rows in _sampled_rows(H, c.S, rng, n_mid=1):
+        osum = np.zeros((H, W), np.uint32)
+        ocnt = np.zeros((H, W), np.uint8)
+        for g, inp in zip(gf, inps):
+            me = {k: v.copy() for k, v in g.items()}
+            me["status"] = np.where(g["status"] >= oracle.CANDIDATE, oracle.CANDIDATE, g["status"]).astype(np.uint8)
+            o = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], K=8, S=c.S, rows=rows)
+            f32_me_compare(me, o, inp, 8, c.S, rows=rows)
+            st = oracle.nnc(me, 1, rows=rows)
+            me["status"] = st
+            st, _ = oracle.frmc(inp["cur"], inp["cur_mask"], inp["ref"], me, K=8, S=c.S, rows=rows)
+            sl = slice(*rows)
+            assert np.array_equal(g["status"][sl], st[sl]), rows
+            me["status"] = st
+            osum, ocnt = oracle.project(me, inp["past_val"], inp["past_mask"], osum, ocnt, rows=rows)
+        sl = slice(*rows)
+        assert np.array_equal(gsum[sl], osum[sl]) and np.array_equal(gcnt[sl], ocnt[sl]), rows

@@ -629,3 +629,40 @@ def test_fullsize_config4_bench_launch_sampled():
             osum, ocnt = oracle.project(me, inp["past_val"], inp["past_mask"], osum, ocnt, rows=rows)
         sl = slice(*rows)
         assert np.array_equal(gsum[sl], osum[sl]) and np.array_equal(gcnt[sl], ocnt[sl]), rows
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_fullsize_u8_bench_launch_sampled(cfg):
+    """The bench's launch on the uint8 configs at full size: qs_me_search_refs over d = 1..3 with the
+    fused cascade and PR, bit-exact against the oracle's chain on sampled rows."""
+    c = synth.CONFIGS[cfg]
+    seq = synth.make_sequence(cfg)
+    t = 3
+    inps = [synth.pair_inputs(seq, t, d) for d in (1, 2, 3)]
+    H, W = c.h, c.w
+    cur = qs.to_plane(inps[0]["cur"], DEV_)
+    msk = qs.to_plane(inps[0]["cur_mask"], DEV_)
+    refs = [qs.to_plane(i["ref"], DEV_) for i in inps]
+    pvs = [qs.to_plane(i["past_val"], DEV_) for i in inps]
+    pms = [qs.to_plane(i["past_mask"], DEV_) for i in inps]
+    outs = [qs.Field.alloc(H, W, False, DEV_) for _ in inps]
+    s, cn = qs.alloc_acc(H, W, DEV_)
+    qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H), qs.make_params(K=8, S=c.S), outs,
+                         fuse=qs.make_checks(), project=(pvs, pms, s, cn))
+    torch.cuda.synchronize()
+    gsum, gcnt = s.cpu().numpy().view(np.uint32), cn.cpu().numpy()
+    gf = []
+    for o in outs:
+        g = o.numpy()
+        g["err"] = g["err"].view(np.uint32)
+        gf.append(g)
+    rng = np.random.default_rng(cfg + 100)
+    for rows in _sampled_rows(H, c.S, rng, n_mid=1):
+        osum = np.zeros((H, W), np.uint32)
+        ocnt = np.zeros((H, W), np.uint8)
+        for g, inp in zip(gf, inps):
+            o, _ = oracle.pair_chain(inp, K=8, S=c.S, check="nnc_frmc", rows=rows)
+            assert_field_equal(g, o, rows=rows, what=f"config {cfg} refs rows {rows}")
+            osum, ocnt = oracle.project(o, inp["past_val"], inp["past_mask"], osum, ocnt, rows=rows)
+        sl = slice(*rows)
+        assert np.array_equal(gsum[sl], osum[sl]) and np.array_equal(gcnt[sl], ocnt[sl]), rows

@@ -37,7 +37,11 @@ METRIC = "ME+consistency-check Mpixel/s (1080p, 1/2/4/8 B200) and % of roofline"
 SM_COUNT = 148
 FP32_LANES_PER_SM = 128          # B200 SM: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md, blackwell guide)
 SM_MAX_MHZ = 1965.0              # clocks.max.sm (B200_PROFILING.md)
-OPS_PER_UNIT = 8                 # D (2) + H (2) + V (2) + argmin (2) per (pixel, candidate)
+# Algorithmic work per (pixel, candidate): SURVEY.md §8(d.3)/(d.4) F-b "Box" basis, 4 ops (the judged
+# basis: roofline.frac); DESIGN.md's per-stage count of the same separable formulation, 8 ops (D 2 +
+# H 2 + V 2 + argmin 2), is reported beside it as roofline.alt.
+OPS_PER_UNIT = 4
+OPS_PER_UNIT_DESIGN = 8
 
 
 def parse():
@@ -162,6 +166,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's init lines (rank count, transports, NVLS) on stderr, so the rank count is checkable
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     cfg = synth.CONFIGS[args.config]
     W, H, K, S = cfg.w, cfg.h, cfg.K, cfg.S
@@ -304,18 +311,24 @@ def run_ours(args):
     units_per_launch = (args.steps * 3 * me_rows * W * n_cand) // me_n if me_n else 0
     achieved = OPS_PER_UNIT * units_per_launch / (me_ms / me_n / 1e3) / 1e12 if me_n else None
     peak = SM_COUNT * FP32_LANES_PER_SM * SM_MAX_MHZ * 1e6 / 1e12
+    # DRAM traffic of one me_box launch of THIS config, from the ncu capture of the bench's own
+    # steady-state loop with --cache-control none (profiles/me_box_traffic_c<cfg>.json); None if absent.
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "me_box_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", f"me_box_traffic_c{args.config}.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    alt = OPS_PER_UNIT_DESIGN * units_per_launch / (me_ms / me_n / 1e3) / 1e12 if me_n else None
     roofline = {"bound": "alu", "kernel": "me_box", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "ops_per_unit": OPS_PER_UNIT, "units_per_launch": units_per_launch,
+                "ops_per_unit": OPS_PER_UNIT, "ops_basis": "SURVEY.md 8(d.3) box ops per (pixel, candidate)",
+                "units_per_launch": units_per_launch,
                 "avg_launch_ms": me_ms / me_n if me_n else None,
                 "share_of_step": me_ms / ms if ms else None,
+                "alt": {"ops_per_unit": OPS_PER_UNIT_DESIGN, "achieved": alt,
+                        "frac": (alt / peak) if alt else None, "basis": "DESIGN.md section 6 per-stage count"},
                 "peak_basis": "148 SM x 128 FP32 lanes x 1965 MHz (guide unit counts and max clock)"}
     kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
 
@@ -519,7 +532,7 @@ def run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32):
 # ---------------------------------------------------------------------------
 # The oracle: cpu_baseline (inside our line) and the --impl reference arm
 # ---------------------------------------------------------------------------
-def oracle_sample(frames, cfg, t, rows):
+def oracle_sample(frames, cfg, t, rows, threads=1):
     """The oracle on a bounded sample: output rows `rows` of frame t, references d = 1..3:
     ME -> NNC -> FRMC -> PR on those rows (timed).  The 2 halo rows of vectors NNC reads are
     computed untimed, as a full-frame run computes them once for the neighbouring rows.
@@ -534,32 +547,54 @@ def oracle_sample(frames, cfg, t, rows):
         cur, msk, ref = frames[t]["cur"], frames[t]["mask"], frames[t - d]["ref"]
         kw = dict(K=K, S=S, min_support=8)
         t0 = time.perf_counter()
-        f = oracle.me_search(cur, msk, ref, rows=(y0, y1), **kw)
+        f = oracle.me_search(cur, msk, ref, rows=(y0, y1), threads=threads, **kw)
         sec += time.perf_counter() - t0
         for hr in ((max(0, y0 - 2), y0), (y1, min(H, y1 + 2))):
             if hr[0] < hr[1]:
-                h = oracle.me_search(cur, msk, ref, rows=hr, **kw)
+                h = oracle.me_search(cur, msk, ref, rows=hr, threads=threads, **kw)
                 for k in f:
                     f[k][hr[0]:hr[1]] = h[k][hr[0]:hr[1]]
         t0 = time.perf_counter()
         f["status"] = oracle.nnc(f, 1, rows=(y0, y1))
-        f["status"], _ = oracle.frmc(cur, msk, ref, f, rows=(y0, y1), **kw)
+        f["status"], _ = oracle.frmc(cur, msk, ref, f, rows=(y0, y1), threads=threads, **kw)
         s, c = oracle.project(f, frames[t - d]["cur"], frames[t - d]["mask"], s, c, rows=(y0, y1))
         sec += time.perf_counter() - t0
     return sec
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(seq, frames, cfg, rows=None):
+    """The oracle timed on the box's host cores: mode 1, one thread (the paper's
+    protocol, "restrict the executions to a single core"); mode 2, the OpenMP row driver
+    on every host core (oracle/omp_driver.c: the same definitions, rows in parallel)."""
     import oracle
     oracle.build()
     H = cfg.h
     rows = rows or (H // 2, H // 2 + 6)
     sec = oracle_sample(frames, cfg, 3, rows)
     px = (rows[1] - rows[0]) * cfg.w
+    ncores = oracle.threads_available()
+    n_rows = min(H - 4, 6 * ncores)
+    r2 = (max(2, H // 2 - n_rows // 2), max(2, H // 2 - n_rows // 2) + n_rows)
+    sec2 = oracle_sample(frames, cfg, 3, r2, threads=ncores)
+    px2 = (r2[1] - r2[0]) * cfg.w
     return {"value": round(px / sec / 1e6, 6), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
             "sample": f"frame t=3 of {cfg.name}, output rows {rows[0]}-{rows[1] - 1} ({rows[1] - rows[0]} of {H}), "
                       f"d=1..3, ME on rows +-2 (NNC halo) -> NNC -> FRMC -> PR; single-threaded C oracle",
-            "seconds": round(sec, 3)}
+            "seconds": round(sec, 3), "cpu_model": cpu_model(),
+            "all_cores": {"value": round(px2 / sec2 / 1e6, 6), "unit": "Mpixel/s", "cores": ncores,
+                          "sample": f"frame t=3, output rows {r2[0]}-{r2[1] - 1} ({n_rows} of {H}), d=1..3, same "
+                                    f"chain through the OpenMP row driver on {ncores} threads",
+                          "seconds": round(sec2, 3)}}
 
 
 def run_reference(args):

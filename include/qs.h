@@ -155,21 +155,29 @@ int qs_workspace_size(const qs_roi *roi, int32_t frame_w, int32_t frame_h, const
  *     T_p(v) = { q = p+o : q in frame, cur_mask(q) = 1, q+v in frame }.
  * The chosen v minimises the mean e/n over admissible candidates (n >=
  * min_support), ties broken by (|alpha|+|beta|, alpha, beta) ascending (R7).
- * Mean comparison: exact for uint8 references; for float32 references the
- * sums are fp32 in a blocked order, the
- * reported err is the fp32 row-major sum of the chosen vector.
+ * Mean comparison: exact for uint8 references (integer cross-multiplication).
+ * For float32 references the result is the definition's in fp32 arithmetic
+ * (R23): terms fl(c - r), |d| or fl(d*d), summed in row-major template order,
+ * compared by fl(e/n), ties by rank -- bit-identical to a sequential
+ * implementation.  The search sums in a faster blocked order and certifies
+ * each winner against an error bound; outputs it cannot certify are
+ * recomputed in the definition's order (
+ * qs_certify_stats counts them).  err is the row-major fp32 sum.
  *
  *   cur, cur_mask  uint8 [rows][cur_pitch]: current sampled frame (values read
  *                  only where cur_mask == 1) and its quarter mask in {0,1}
  *   ref            uint8 or float32 [rows][ref_pitch]: previous reconstruction
- *   roi            row window (NULL = whole frame); buffers must hold rows
+ *   roi            row window (required: it carries the frame size); buffers must hold rows
  *                  [y_begin - K/2 - S - 2, y_end + K + S + 2) clipped to the frame
  *                  (the +2 covers the NNC halo when `fuse` is set)
  *   fuse           NULL = ME only (statuses NOT_TARGET / INVALID / CANDIDATE);
  *                  otherwise the checks of qs_checks run on rows [y_begin, y_end).
- *                  NNC needs vectors 2 rows beyond the roi: ME then also fills
+ *                  NNC needs vectors 2 rows beyond the roi: ME then also runs on
  *                  rows [y_begin-2, y_end+2) (clipped to the frame), which the
- *                  field buffers must hold; those halo rows keep ME statuses.
+ *                  field buffers must hold, but only rows [y_begin, y_end) of
+ *                  `out` are written (the halo vectors stay in the workspace),
+ *                  so adjacent rois may share one field buffer and run on
+ *                  different streams.
  *   out            field planes (buffer window of the roi)
  *   eval_count     nullable device counter; FRMC adds |offsets|^2 per checked
  *                  entry (definitional count, R17)
@@ -288,7 +296,11 @@ int qs_nnc_mode(qs_field *io, const qs_roi *roi, int32_t threshold, int32_t mode
  * and past_mask(q) == 1: sum(p) += past_val(q), cnt(p) += 1.  ACCUMULATES into
  * caller-zeroed sum (uint32) / cnt (uint8) planes [rows][acc_pitch elements],
  * so successive calls for d = 1, 2, 3 average across references.  past_* must
- * hold rows [y_begin - S, y_end + S) clipped (|alpha| <= S).
+ * hold rows [y_begin - S, y_end + S) clipped (|alpha| <= S).  The call has no S
+ * to validate that against: an ACCEPTED entry whose q = p+v lies outside the
+ * past buffers' row window [buf_y0, buf_y0 + buf_rows) is NOT projected (no
+ * error is returned), so a caller passing too few past rows gets smaller
+ * sum / cnt for those entries.
  * ------------------------------------------------------------------------- */
 int qs_project(const qs_field *f, const uint8_t *past_val, const uint8_t *past_mask, int64_t past_pitch,
                const qs_roi *roi, uint32_t *sum, uint8_t *cnt, int64_t acc_pitch, void *stream);
@@ -305,6 +317,15 @@ int qs_project(const qs_field *f, const uint8_t *past_val, const uint8_t *past_m
 int qs_profile_enable(int32_t on);
 int qs_profile_read(const char *kernel, double *total_ms, int64_t *launches);
 int qs_profile_reset(void);
+
+/* ---------------------------------------------------------------------------
+ * qs_certify_stats -- float references only: the number of
+ * outputs (forward targets and reverse positions) whose approximate argmin could not be certified
+ * and were recomputed exactly in the definition's arithmetic, summed over every call on the current
+ * device since the last reset.  Synchronises the device.  reset != 0 zeroes the counter after
+ * reading it.  QS_EINVAL for a NULL pointer, QS_ECUDA if the device access fails.
+ * ------------------------------------------------------------------------- */
+int qs_certify_stats(int64_t *rechecked, int32_t reset);
 
 /* Thread-local message describing the last non-QS_OK return on this thread. */
 const char *qs_last_error(void);

@@ -36,11 +36,19 @@ NOT_TARGET, INVALID, CANDIDATE, ACCEPTED, REJECTED = 0, 1, 2, 3, 4
 REF_U8, REF_F32, REF_F32_ACC64 = 0, 1, 2
 
 
+_OMP_SRC = os.path.join(_HERE, "omp_driver.c")
+_OMP_LIB = os.path.join(_HERE, "liboracle_omp.so")
+_CFLAGS = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall"]
+
+
 def build(force: bool = False) -> str:
-    """Compile the plain-C oracle (-O2, no FMA contraction, no fast-math)."""
+    """Compile the plain-C oracle (-O2, no FMA contraction, no fast-math), and the OpenMP row driver
+    (omp_driver.c, linked with the same oracle.c into liboracle_omp.so)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-                               "-Wall", "-o", _LIB, _SRC])
+        subprocess.check_call(_CFLAGS + ["-o", _LIB, _SRC])
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_OMP_SRC))
+    if force or not os.path.exists(_OMP_LIB) or os.path.getmtime(_OMP_LIB) < newest:
+        subprocess.check_call(_CFLAGS + ["-fopenmp", "-o", _OMP_LIB, _SRC, _OMP_SRC])
     return _LIB
 
 
@@ -51,6 +59,28 @@ class _Params(C.Structure):
 
 
 _lib = None
+_omp = None
+
+
+def omp_lib():
+    """The OpenMP row driver (same definitions; rows in parallel)."""
+    global _omp
+    if _omp is None:
+        build()
+        _omp = C.CDLL(_OMP_LIB)
+        P = C.POINTER(_Params)
+        vp = C.c_void_p
+        i32 = C.c_int32
+        _omp.or_threads_available.argtypes = []
+        _omp.or_me_search_omp.argtypes = [P, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32]
+        _omp.or_frmc_omp.argtypes = [P, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, i32]
+        _omp.or_rmc_omp.argtypes = [P, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, i32, i32]
+        _omp.or_rme_omp.argtypes = [P, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, i32]
+    return _omp
+
+
+def threads_available() -> int:
+    return int(omp_lib().or_threads_available())
 
 
 def lib():
@@ -106,8 +136,10 @@ def rank_list(S: int):
     return a, b
 
 
-def me_search(cur, cur_mask, ref, K=8, S=8, min_support=8, ssd=False, ref_mode=None, rows=None):
-    """ME over target rows ``rows=(y0, y1)`` (default: all). Returns the field planes."""
+def me_search(cur, cur_mask, ref, K=8, S=8, min_support=8, ssd=False, ref_mode=None, rows=None, threads=1):
+    """ME over target rows ``rows=(y0, y1)`` (default: all). Returns the field planes.
+
+    threads > 1 runs the rows through the OpenMP driver (the same definitions, one row per call)."""
     cur = _c(cur, np.uint8)
     mask = _c(cur_mask, np.uint8)
     P, ref_mode = _params(cur, ref, K, S, min_support, ssd, ref_mode)
@@ -117,14 +149,16 @@ def me_search(cur, cur_mask, ref, K=8, S=8, min_support=8, ssd=False, ref_mode=N
     f = dict(alpha=np.zeros((H, W), np.int8), beta=np.zeros((H, W), np.int8),
              err=np.zeros((H, W), _err_dtype(ref_mode)), count=np.zeros((H, W), np.uint8),
              status=np.zeros((H, W), np.uint8))
-    r = lib().or_me_search(C.byref(P), _p(cur), _p(mask), _p(ref), y0, y1, _p(f["alpha"]), _p(f["beta"]),
-                           _p(f["err"]), _p(f["count"]), _p(f["status"]))
+    args = [C.byref(P), _p(cur), _p(mask), _p(ref), y0, y1, _p(f["alpha"]), _p(f["beta"]),
+            _p(f["err"]), _p(f["count"]), _p(f["status"])]
+    r = omp_lib().or_me_search_omp(*args, int(threads)) if threads > 1 else lib().or_me_search(*args)
     if r != 0:
         raise ValueError(f"or_me_search failed: {r}")
     return f
 
 
-def _check_call(fn, name, cur, cur_mask, ref, field, K, S, min_support, ssd, ref_mode, rows, extra_pre, extra_post):
+def _check_call(fn, name, cur, cur_mask, ref, field, K, S, min_support, ssd, ref_mode, rows, extra_pre, extra_post,
+                threads=1):
     cur = _c(cur, np.uint8)
     mask = _c(cur_mask, np.uint8)
     P, ref_mode = _params(cur, ref, K, S, min_support, ssd, ref_mode)
@@ -137,6 +171,9 @@ def _check_call(fn, name, cur, cur_mask, ref, field, K, S, min_support, ssd, ref
     args = [C.byref(P), _p(cur), _p(mask), _p(ref)] + extra_pre + [
         y0, y1, _p(_c(field["alpha"], np.int8)), _p(_c(field["beta"], np.int8)), _p(err),
         _p(_c(field["count"], np.uint8)), _p(st), _p(ev)] + extra_post
+    if threads > 1:
+        fn = getattr(omp_lib(), name + "_omp")
+        args = args + [int(threads)]
     r = fn(*args)
     if r != 0:
         raise ValueError(f"{name} failed: {r}")
@@ -144,23 +181,24 @@ def _check_call(fn, name, cur, cur_mask, ref, field, K, S, min_support, ssd, ref
 
 
 def frmc(cur, cur_mask, ref, field, offsets=(-7, -3, -1, 0, 1, 3, 7), K=8, S=8, min_support=8, ssd=False,
-         ref_mode=None, rows=None, verify_p4=True):
+         ref_mode=None, rows=None, verify_p4=True, threads=1):
     """FRMC. Returns (new status plane, definitional evaluation count)."""
     offs = np.asarray(offsets, np.int32)
     return _check_call(lib().or_frmc, "or_frmc", cur, cur_mask, ref, field, K, S, min_support, ssd, ref_mode,
-                       rows, [_p(offs), len(offs)], [int(verify_p4)])
+                       rows, [_p(offs), len(offs)], [int(verify_p4)], threads)
 
 
-def rmc(cur, cur_mask, ref, field, K=8, S=8, min_support=8, ssd=False, ref_mode=None, rows=None, verify_p4=True):
+def rmc(cur, cur_mask, ref, field, K=8, S=8, min_support=8, ssd=False, ref_mode=None, rows=None, verify_p4=True,
+        threads=1):
     """RMC. Returns (new status plane, evaluation count)."""
     return _check_call(lib().or_rmc, "or_rmc", cur, cur_mask, ref, field, K, S, min_support, ssd, ref_mode,
-                       rows, [], [int(verify_p4)])
+                       rows, [], [int(verify_p4)], threads)
 
 
-def rme(cur, cur_mask, ref, field, K=8, S=8, min_support=8, ssd=False, ref_mode=None, rows=None):
+def rme(cur, cur_mask, ref, field, K=8, S=8, min_support=8, ssd=False, ref_mode=None, rows=None, threads=1):
     """RME. Returns (new status plane, evaluation count)."""
     return _check_call(lib().or_rme, "or_rme", cur, cur_mask, ref, field, K, S, min_support, ssd, ref_mode,
-                       rows, [], [])
+                       rows, [], [], threads)
 
 
 def nnc(field, threshold=1, rows=None, pairs=False):
@@ -232,7 +270,7 @@ def cost_rev(cur, cur_mask, ref, y, x, a, b, K=8, min_support=8, ssd=False, ref_
 # R16 cascade, R19 references)
 # --------------------------------------------------------------------------
 def pair_chain(inp: dict, K=8, S=8, min_support=8, ssd=False, check="nnc_frmc", threshold=1,
-               offsets=(-7, -3, -1, 0, 1, 3, 7), rows=None, ref_mode=None):
+               offsets=(-7, -3, -1, 0, 1, 3, 7), rows=None, ref_mode=None, threads=1):
     """ME -> check -> (field, evals) for one (t, d) pair.
 
     check: none | rme | rmc | frmc | nnc | nnc_frmc (the paper's cascade: NNC
@@ -242,20 +280,21 @@ def pair_chain(inp: dict, K=8, S=8, min_support=8, ssd=False, check="nnc_frmc", 
     H = inp["cur"].shape[0]
     mrows = None if rows is None else (max(0, rows[0] - 2), min(H, rows[1] + 2))
     kw = dict(K=K, S=S, min_support=min_support, ssd=ssd, ref_mode=ref_mode)
-    f = me_search(inp["cur"], inp["cur_mask"], inp["ref"], rows=mrows, **kw)
+    kt = dict(kw, threads=threads)
+    f = me_search(inp["cur"], inp["cur_mask"], inp["ref"], rows=mrows, **kt)
     ev = 0
     if check == "none":
         pass
     elif check == "rme":
-        f["status"], ev = rme(inp["cur"], inp["cur_mask"], inp["ref"], f, rows=rows, **kw)
+        f["status"], ev = rme(inp["cur"], inp["cur_mask"], inp["ref"], f, rows=rows, **kt)
     elif check == "rmc":
-        f["status"], ev = rmc(inp["cur"], inp["cur_mask"], inp["ref"], f, rows=rows, **kw)
+        f["status"], ev = rmc(inp["cur"], inp["cur_mask"], inp["ref"], f, rows=rows, **kt)
     elif check == "frmc":
-        f["status"], ev = frmc(inp["cur"], inp["cur_mask"], inp["ref"], f, offsets=offsets, rows=rows, **kw)
+        f["status"], ev = frmc(inp["cur"], inp["cur_mask"], inp["ref"], f, offsets=offsets, rows=rows, **kt)
     elif check in ("nnc", "nnc_frmc"):
         f["status"] = nnc(f, threshold, rows=rows)
         if check == "nnc_frmc":
-            f["status"], ev = frmc(inp["cur"], inp["cur_mask"], inp["ref"], f, offsets=offsets, rows=rows, **kw)
+            f["status"], ev = frmc(inp["cur"], inp["cur_mask"], inp["ref"], f, offsets=offsets, rows=rows, **kt)
     else:
         raise ValueError(check)
     return f, ev

@@ -93,6 +93,8 @@ def lib() -> C.CDLL:
         L.qs_project.argtypes = [P(qs_field), vp, vp, i64, P(qs_roi), vp, vp, i64, vp]
         for f in ("qs_workspace_size", "qs_me_search", "qs_me_search_refs", "qs_reverse_check", "qs_frmc", "qs_nnc", "qs_nnc_mode", "qs_project"):
             getattr(L, f).restype = C.c_int
+        L.qs_certify_stats.argtypes = [P(C.c_int64), i32]
+        L.qs_certify_stats.restype = C.c_int
         L.qs_profile_enable.argtypes = [i32]
         L.qs_profile_read.argtypes = [C.c_char_p, P(C.c_double), P(C.c_int64)]
         L.qs_profile_reset.argtypes = []
@@ -136,7 +138,14 @@ def qs_profile_reset():
     lib().qs_profile_reset()
 
 
-PROFILE_KERNELS = ("me_box", "epilogue", "finalize", "nnc", "revgrid", "rme_decide", "project")
+PROFILE_KERNELS = ("me_box", "epilogue", "finalize", "nnc", "revgrid", "rme_decide", "project", "certify")
+
+
+def qs_certify_stats(reset: bool = False) -> int:
+    """Float references: outputs recomputed exactly by the certify kernel since the last reset."""
+    n = C.c_int64(0)
+    _check(lib().qs_certify_stats(C.byref(n), int(reset)))
+    return n.value
 
 
 def _check(rc: int):

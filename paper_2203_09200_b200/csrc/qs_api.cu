@@ -43,8 +43,9 @@ std::map<std::pair<int, int>, qs::CandTables *> g_tabs;
 // ---------------------------------------------------------------------------
 // Profiler: CUDA events around each launch, on the launch stream.
 // ---------------------------------------------------------------------------
-enum ProfKernel { P_ME_BOX = 0, P_FINALIZE, P_NNC, P_REVGRID, P_RME_DECIDE, P_PROJECT, P_EPILOGUE, P_COUNT };
-const char *kProfNames[P_COUNT] = {"me_box", "finalize", "nnc", "revgrid", "rme_decide", "project", "epilogue"};
+enum ProfKernel { P_ME_BOX = 0, P_FINALIZE, P_NNC, P_REVGRID, P_RME_DECIDE, P_PROJECT, P_EPILOGUE, P_CERTIFY, P_COUNT };
+const char *kProfNames[P_COUNT] = {"me_box", "finalize", "nnc", "revgrid", "rme_decide", "project", "epilogue",
+                                   "certify"};
 
 // {-7,-3,-1,0,1,3,7}, in any order.
 bool is_paper_offsets(const int8_t *o, int n) {
@@ -217,11 +218,21 @@ int check_field(const qs_field *f, int W, bool need_err_count) {
 
 FieldView view(const qs_field *f) { return FieldView{f->alpha, f->beta, f->err, f->count, f->status, f->pitch}; }
 
+size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 size_t me_keys_bytes(const Roi &r) {
     return sizeof(unsigned long long) * (size_t)std::max(0, std::min(r.H, r.y1 + 2) - std::max(0, r.y0 - 2)) * r.W;
 }
 size_t rme_keys_bytes(const Roi &r, int S) {
     return sizeof(unsigned long long) * (size_t)(r.y1 - r.y0 + 2 * S) * (size_t)(r.W + 2 * S);
+}
+// Workspace slot: the 64-bit key plane, then (float references) the 32-bit second plane of the
+// certified argmin.  qs_me_search_refs lays out the key planes of
+// its n slots first and their second planes after them.
+// qs_me_search with K != 8 and NNC also keeps a scratch field (8 B per pixel, like the keys) for the
+// ME rows [y0-2, y1+2): NNC reads the halo rows there and only the roi's rows reach the caller's field.
+size_t ws_slot_bytes(const Roi &r, int S) {
+    const size_t me = me_keys_bytes(r), rme = rme_keys_bytes(r, S);
+    return std::max(2 * al256(me) + al256(me / 2), al256(rme) + al256(rme / 2));
 }
 
 BoxArgs box_args(const Roi &r, const uint8_t *cur, const uint8_t *mask, int64_t cur_pitch, const void *ref,
@@ -252,6 +263,42 @@ int check_offsets(const int8_t *offs, int n, int S) {
     }
     if (!has0) return fail(QS_EINVAL, "offsets must contain 0");
     return QS_OK;
+}
+
+// Certificate + exact recompute of the float argmin (certify.cu) over the keys of a box launch.
+int run_certify(const BoxArgs &a, int K, bool ssd, bool reverse, const CandTables *t, cudaStream_t s) {
+    CertifyArgs c{};
+    c.cur = a.cur;
+    c.mask = a.mask;
+    c.ref = a.ref;
+    c.ssd = ssd;
+    c.K = K;
+    c.W = a.W;
+    c.H = a.H;
+    c.buf_y0 = a.buf_y0;
+    c.buf_rows = a.buf_rows;
+    c.min_support = a.min_support;
+    c.oy0 = a.oy0;
+    c.oy1 = a.oy1;
+    c.ox0 = a.ox0;
+    c.ox1 = a.ox1;
+    c.key_pitch = a.key_pitch;
+    c.reverse = reverse;
+    c.n_ref = a.n_ref > 0 ? a.n_ref : 1;
+    for (int i = 0; i < c.n_ref; ++i) {
+        c.ref_p[i] = a.n_ref > 0 ? a.ref_p[i] : a.ref.p;
+        c.keys_p[i] = a.n_ref > 0 ? a.keys_p[i] : a.keys;
+        c.s2_p[i] = a.n_ref > 0 ? a.s2_p[i] : a.s2;
+    }
+    c.canon = t->canon;
+    c.n_cand = t->n;
+    c.rechecked = rechecked_counter();
+    cudaError_t e;
+    {
+        ProfScope ps(P_CERTIFY, s);
+        e = launch_certify(c, s);
+    }
+    return e == cudaSuccess ? QS_OK : cuda_fail(e, "certify launch");
 }
 
 int run_frmc(const Roi &r, const uint8_t *cur, const uint8_t *mask, int64_t cur_pitch, const void *ref,
@@ -301,8 +348,7 @@ int qs_workspace_size(const qs_roi *roi, int32_t frame_w, int32_t frame_h, const
     if (frame_w != r.W || frame_h != r.H) return fail(QS_EDIM, "frame size disagrees with roi");
     if ((rc = check_params(p))) return rc;
     if (!bytes) return fail(QS_EINVAL, "bytes is NULL");
-    size_t b = std::max(me_keys_bytes(r), rme_keys_bytes(r, p->S));
-    *bytes = (b + 255) & ~size_t(255);
+    *bytes = ws_slot_bytes(r, p->S);
     return QS_OK;
 }
 
@@ -324,7 +370,10 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     const int K = p->K_h, KL = K / 2, KR = K - 1 - KL;
     if ((rc = need_rows(r, lo, hi, "field")) || (rc = need_rows(r, lo - KL - p->S, hi + KR + p->S, "ME inputs")))
         return rc;
-    const size_t need = me_keys_bytes(r);
+    const bool f32 = p->ref_type == QS_REF_F32;
+    const size_t kb = me_keys_bytes(r);
+    const bool scratch = K != 8 && nnc;   // finalize + NNC through a scratch field (ws_slot_bytes)
+    const size_t need = scratch ? 2 * al256(kb) + al256(kb / 2) : f32 ? al256(kb) + al256(kb / 2) : kb;
     if (!workspace || !aligned16(workspace) || workspace_bytes < need)
         return fail(QS_EDIM, "workspace: need %zu bytes (16-byte aligned), got %zu", need, workspace_bytes);
     const char *terr = nullptr;
@@ -334,7 +383,9 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     if (r.y1 <= r.y0 || hi <= lo) return QS_OK;   // empty roi: nothing is written
 
     auto *keys = static_cast<unsigned long long *>(workspace);
+    unsigned *s2 = f32 ? reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + al256(kb)) : nullptr;
     cudaError_t e = cudaMemsetAsync(keys, 0xff, sizeof(unsigned long long) * (size_t)(hi - lo) * r.W, s);
+    if (e == cudaSuccess && f32) e = cudaMemsetAsync(s2, 0xff, sizeof(unsigned) * (size_t)(hi - lo) * r.W, s);
     if (e != cudaSuccess) return cuda_fail(e, "memset keys");
     BoxArgs a = box_args(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, t);
     a.oy0 = lo;
@@ -345,11 +396,13 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     a.tiles_y = (hi - lo + kTY - 1) / kTY;
     a.keys = keys;
     a.key_pitch = r.W;
+    a.s2 = s2;
     {
         ProfScope ps(P_ME_BOX, s);
         e = launch_box(a, K, p->err == QS_SSD, false, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "me_box launch");
+    if (f32 && (rc = run_certify(a, K, p->err == QS_SSD, false, t, s))) return rc;
 
     if (K == 8) {
         // Fused epilogue: finalize + NNC + FRMC (the paper's offsets, in any order) in one launch.
@@ -409,12 +462,21 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     fa.keys = keys;
     fa.key_pitch = r.W;
     fa.canon = t->canon;
-    fa.alpha = out->alpha;
-    fa.beta = out->beta;
-    fa.err = out->err;
-    fa.count = out->count;
-    fa.status = out->status;
-    fa.fpitch = out->pitch;
+    // Without NNC the ME rows are the roi's: finalize straight into the caller's field.  With NNC the
+    // rows [lo, hi) go to a scratch field (the halo rows belong to the neighbouring bands' calls), NNC
+    // decides [y0, y1) there and those rows are copied out.
+    char *sc = static_cast<char *>(workspace) + al256(kb) + al256(kb / 2);
+    const int64_t sn = (int64_t)(hi - lo) * r.W;
+    qs_field tmp{reinterpret_cast<int8_t *>(sc), reinterpret_cast<int8_t *>(sc + sn), sc + 4 * sn,
+                 reinterpret_cast<uint8_t *>(sc + 2 * sn), reinterpret_cast<uint8_t *>(sc + 3 * sn), r.W};
+    const qs_field *dst = scratch ? &tmp : out;
+    fa.alpha = dst->alpha;
+    fa.beta = dst->beta;
+    fa.err = dst->err;
+    fa.count = dst->count;
+    fa.status = dst->status;
+    fa.fpitch = dst->pitch;
+    fa.field_y0 = scratch ? lo : r.b0;
     {
         ProfScope ps(P_FINALIZE, s);
         e = launch_finalize(fa, s);
@@ -424,9 +486,23 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     if (nnc) {
         {
             ProfScope ps(P_NNC, s);
-            e = launch_nnc(view(out), r.W, r.H, r.b0, r.br, r.y0, r.y1, fuse->nnc_threshold, fuse->nnc, s);
+            e = launch_nnc(view(&tmp), r.W, r.H, lo, hi - lo, r.y0, r.y1, fuse->nnc_threshold, fuse->nnc, s);
         }
         if (e != cudaSuccess) return cuda_fail(e, "nnc launch");
+        const int nr = r.y1 - r.y0;
+        const size_t so = (size_t)(r.y0 - lo) * r.W, dof = (size_t)(r.y0 - r.b0) * out->pitch;
+        const size_t ow = (size_t)out->pitch;
+        e = cudaMemcpy2DAsync(out->alpha + dof, ow, tmp.alpha + so, r.W, r.W, nr, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(out->beta + dof, ow, tmp.beta + so, r.W, r.W, nr, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(out->count + dof, ow, tmp.count + so, r.W, r.W, nr, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(out->status + dof, ow, tmp.status + so, r.W, r.W, nr, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(static_cast<char *>(out->err) + 4 * dof, 4 * ow, static_cast<char *>(tmp.err) + 4 * so,
+                                  4 * (size_t)r.W, 4 * (size_t)r.W, nr, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "copy of the roi rows");
     }
     if (frmc) {
         if ((rc = run_frmc(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, fuse->offsets, fuse->n_offsets, 0, out,
@@ -465,6 +541,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
                     slot * (size_t)n_refs, n_refs, slot, workspace_bytes);
     char *ws = static_cast<char *>(workspace);
     const bool nnc = fuse && fuse->nnc, frmc = fuse && fuse->frmc;
+    if (frmc && (rc = check_offsets(fuse->offsets, fuse->n_offsets, p->S))) return rc;   // before reading them
     const bool paper = frmc && is_paper_offsets(fuse->offsets, fuse->n_offsets);
     // The single-launch path covers the fused K = 8 epilogue; everything else runs slot by slot.
     if (p->K_h != 8 || (frmc && !paper)) {
@@ -499,10 +576,13 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
         if (!t) return fail(QS_ECUDA, "%s", terr);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         if (r.y1 <= r.y0 || hi <= lo) return QS_OK;
-        const size_t kb = me_keys_bytes(r);
+        const size_t kb = me_keys_bytes(r), kba = al256(kb), s2a = al256(kb / 2);
+        const bool f32 = p->ref_type == QS_REF_F32;
         char *wg = ws + slot * i0;
-        // Key planes of the group's slots (slot i at wg + i * slot; one memset over the span).
-        cudaError_t e = cudaMemsetAsync(wg, 0xff, slot * (n - 1) + kb, s);
+        // The group's n slots: key planes at wg + i * kba, then (float) second planes at
+        // wg + n * kba + i * s2a (within the n * slot bytes of the group); one memset per span.
+        cudaError_t e = cudaMemsetAsync(wg, 0xff, kba * (n - 1) + kb, s);
+        if (e == cudaSuccess && f32) e = cudaMemsetAsync(wg + n * kba, 0xff, s2a * (n - 1) + kb / 2, s);
         if (e != cudaSuccess) return cuda_fail(e, "memset keys");
         BoxArgs a = box_args(r, cur, cur_mask, cur_pitch, refs[i0], ref_pitch, p, t);
         a.oy0 = lo;
@@ -516,13 +596,16 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
         a.n_ref = n;
         for (int i = 0; i < n; ++i) {
             a.ref_p[i] = static_cast<const uint8_t *>(refs[i0 + i]);
-            a.keys_p[i] = reinterpret_cast<unsigned long long *>(wg + slot * i);
+            a.keys_p[i] = reinterpret_cast<unsigned long long *>(wg + kba * i);
+            a.s2_p[i] = f32 ? reinterpret_cast<unsigned *>(wg + n * kba + s2a * i) : nullptr;
         }
+        a.s2 = a.s2_p[0];
         {
             ProfScope ps(P_ME_BOX, s);
             e = launch_box(a, 8, p->err == QS_SSD, false, s);
         }
         if (e != cudaSuccess) return cuda_fail(e, "me_box launch");
+        if (f32 && (rc = run_certify(a, 8, p->err == QS_SSD, false, t, s))) return rc;
         EpiArgs g{};
         g.cur = a.cur;
         g.mask = a.mask;
@@ -598,12 +681,16 @@ int qs_reverse_check(int32_t mode, const uint8_t *cur, const uint8_t *cur_mask, 
         return run_frmc(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, nullptr, 0, 1, io, eval_count, s);
     }
     if ((rc = need_rows(r, r.y0 - 2 * S - KL, r.y1 + 2 * S + KR, "RME inputs"))) return rc;
-    const size_t need = rme_keys_bytes(r, S);
+    const bool f32 = p->ref_type == QS_REF_F32;
+    const size_t kb = rme_keys_bytes(r, S);
+    const size_t need = f32 ? al256(kb) + al256(kb / 2) : kb;
     if (!workspace || !aligned16(workspace) || workspace_bytes < need)
         return fail(QS_EDIM, "workspace: need %zu bytes (16-byte aligned), got %zu", need, workspace_bytes);
     if (r.y1 <= r.y0) return QS_OK;
     auto *keys = static_cast<unsigned long long *>(workspace);
-    cudaError_t e = cudaMemsetAsync(keys, 0xff, need, s);
+    unsigned *s2 = f32 ? reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + al256(kb)) : nullptr;
+    cudaError_t e = cudaMemsetAsync(keys, 0xff, kb, s);
+    if (e == cudaSuccess && f32) e = cudaMemsetAsync(s2, 0xff, kb / 2, s);
     if (e != cudaSuccess) return cuda_fail(e, "memset keys");
     BoxArgs a = box_args(r, cur, cur_mask, cur_pitch, ref, ref_pitch, p, t);
     a.oy0 = r.y0 - S;
@@ -614,11 +701,13 @@ int qs_reverse_check(int32_t mode, const uint8_t *cur, const uint8_t *cur_mask, 
     a.tiles_y = (r.y1 - r.y0 + 2 * S + kTY - 1) / kTY;
     a.keys = keys;
     a.key_pitch = r.W + 2 * S;
+    a.s2 = s2;
     {
         ProfScope ps(P_ME_BOX, s);
         e = launch_box(a, K, p->err == QS_SSD, true, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "rme box launch");
+    if (f32 && (rc = run_certify(a, K, p->err == QS_SSD, true, t, s))) return rc;
     RmeDecideArgs d{};
     d.W = r.W;
     d.H = r.H;
@@ -743,6 +832,19 @@ int qs_profile_read(const char *kernel, double *total_ms, int64_t *launches) {
     }
     *total_ms = t;
     *launches = n;
+    return QS_OK;
+}
+
+int qs_certify_stats(int64_t *rechecked, int32_t reset) {
+    if (!rechecked) return fail(QS_EINVAL, "rechecked is NULL");
+    unsigned long long *c = rechecked_counter();
+    if (!c) return fail(QS_ECUDA, "certify counter unavailable");
+    unsigned long long v = 0;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(&v, c, sizeof v, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && reset) e = cudaMemset(c, 0, sizeof v);
+    if (e != cudaSuccess) return cuda_fail(e, "certify counter");
+    *rechecked = (int64_t)v;
     return QS_OK;
 }
 

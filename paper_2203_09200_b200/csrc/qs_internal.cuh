@@ -76,7 +76,42 @@ struct BoxArgs {
     int n_ref;                       // slots per launch: CTA b works on slot b % n_ref (0 -> 1)
     const uint8_t *ref_p[kMaxRefs];
     unsigned long long *keys_p[kMaxRefs];
+    // Float references only (certified argmin): per output the
+    // smallest approximate mean of every candidate other than the merged winner, as non-negative
+    // float bits ([oy1-oy0][key_pitch], 0xffffffff = none).  nullptr for uint8 references.
+    unsigned *s2;
+    unsigned *s2_p[kMaxRefs];
 };
+
+// Certified float argmin.  The float consumers track, per output,
+// the two smallest KEYED approximate means: the low kKeyBits of the fp32 bits replaced by the
+// candidate's chunk-list position (< 512), so one FMNMX orders (truncated mean, position) and the
+// winner's rank decodes from the key.  Truncation moves a value by < 2^-14 relative; with the fp32
+// sum errors of both sides (<= 2^-17 relative) the winner w is the oracle's whenever every other
+// candidate's truncated value exceeds w's by the factor (1 + kCertEps).
+constexpr unsigned kKeyBits = 511u;
+constexpr float kCertEps = 1.0f / 8192.0f;   // 2^-13
+constexpr float kInadmissible = 3.0e38f;     // finite: keyed bits stay finite (never NaN)
+constexpr float kAdmissibleMax = 1.0e38f;
+
+// Forward / reverse certification and exact recompute of uncertain outputs (certify.cu).
+struct CertifyArgs {
+    Plane cur, mask, ref;
+    int ssd, K;
+    int W, H, buf_y0, buf_rows, min_support;
+    int oy0, oy1, ox0, ox1;          // key domain (frame coordinates)
+    int64_t key_pitch;
+    int reverse;                     // 0: forward ME keys (targets only), 1: dense reverse keys (RME)
+    int n_ref;
+    const uint8_t *ref_p[kMaxRefs];
+    unsigned long long *keys_p[kMaxRefs];
+    const unsigned *s2_p[kMaxRefs];
+    const int32_t *canon;
+    int n_cand;
+    unsigned long long *rechecked;   // nullable device counter: outputs recomputed exactly
+};
+cudaError_t launch_certify(const CertifyArgs &a, cudaStream_t s);
+unsigned long long *rechecked_counter();   // current device's counter (nullptr on failure)
 
 // Launchers (me_box.cu).  Return cudaError_t of the launch.
 cudaError_t launch_box(const BoxArgs &a, int K, bool ssd, bool reverse, cudaStream_t s);
@@ -93,7 +128,8 @@ struct FinalizeArgs {
     int8_t *alpha, *beta;
     void *err;
     uint8_t *count, *status;
-    int64_t fpitch;                  // field pitch (elements); field row 0 == global buf_y0
+    int64_t fpitch;                  // field pitch (elements); field row 0 == global field_y0
+    int field_y0;
 };
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t s);
 

@@ -107,30 +107,3 @@ def assert_field_equal(g, o, rows=None, what=""):
         assert np.array_equal(ge.astype(np.float32).view(np.uint32), oe.astype(np.float32).view(np.uint32)), what
     else:
         assert np.array_equal(ge.astype(np.uint64), oe.astype(np.uint64)), what
-
-
-def f32_me_compare(g, o, inp, K, S, min_support=8, ssd=False, rows=None, rel=1e-5):
-    """Float-reference parity (north_star): statuses equal; vectors equal except at near-ties, where the
-    oracle's fp32 means of both vectors are within the rounding bound; err of equal vectors within 1e-5
-    relative (here it is the same row-major fp32 sum, so bit-equal).  Returns the near-tie positions."""
-    sl = slice(None) if rows is None else slice(*rows)
-    assert np.array_equal(g["status"][sl], o["status"][sl])
-    cand = o["status"][sl] == oracle.CANDIDATE
-    same = cand & (g["alpha"][sl] == o["alpha"][sl]) & (g["beta"][sl] == o["beta"][sl])
-    ge = g["err"][sl][same].astype(np.float64)
-    oe = o["err"][sl][same].astype(np.float64)
-    assert np.all(np.abs(ge - oe) <= rel * np.maximum(oe, 1e-30)), "err beyond 1e-5 relative"
-    assert np.array_equal(g["count"][sl][same], o["count"][sl][same])
-    ties = []
-    y_off = 0 if rows is None else rows[0]
-    for yy, xx in np.argwhere(cand & ~same):
-        y = yy + y_off
-        e1, n1 = oracle.cost_fwd(inp["cur"], inp["cur_mask"], inp["ref"], y, xx, int(g["alpha"][y, xx]),
-                                 int(g["beta"][y, xx]), K=K, min_support=min_support, ssd=ssd)
-        e2, n2 = oracle.cost_fwd(inp["cur"], inp["cur_mask"], inp["ref"], y, xx, int(o["alpha"][y, xx]),
-                                 int(o["beta"][y, xx]), K=K, min_support=min_support, ssd=ssd)
-        m1, m2 = e1 / n1, e2 / n2
-        # fp32 sums of <= 81 non-negative terms: relative error <= 81 * 2^-24 ~ 4.8e-6 each.
-        assert n1 >= min_support and abs(m1 - m2) <= 1e-5 * max(m2, 1e-6), (y, xx, m1, m2)
-        ties.append((int(y), int(xx)))
-    return ties

@@ -529,3 +529,19 @@ def test_p7b_nnc_pairs_equals_centre_reading_on_the_p7_fixtures(golden):
         f = dict(alpha=_arr(case["alpha"], np.int8), beta=_arr(case["beta"], np.int8),
                  status=_arr(case["status"], np.uint8))
         assert np.array_equal(oracle.nnc(f, pairs=True), oracle.nnc(f, pairs=False)), case["name"]
+
+
+def test_omp_row_driver_equals_sequential_oracle():
+    """oracle/omp_driver.c adds no arithmetic: rows through the OpenMP driver (one definition call per
+    row) give the sequential oracle's planes and counts for u8 and f32, ME and every reverse check."""
+    for f32 in (False, True):
+        inp = synth.rank_free_random_instance(31 + f32, 48, 40, ref_f32=f32, smooth=True)
+        kw = dict(K=8, S=8)
+        a = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], **kw)
+        b = oracle.me_search(inp["cur"], inp["cur_mask"], inp["ref"], threads=4, **kw)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+        for fn in (oracle.frmc, oracle.rmc, oracle.rme):
+            s1, e1 = fn(inp["cur"], inp["cur_mask"], inp["ref"], a, **kw)
+            s2, e2 = fn(inp["cur"], inp["cur_mask"], inp["ref"], a, threads=4, **kw)
+            assert np.array_equal(s1, s2) and e1 == e2, fn.__name__

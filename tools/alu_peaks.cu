@@ -22,13 +22,33 @@ constexpr int CH = 8;
         if (s == (T)seed) out[threadIdx.x] = s;                                         \
     }
 
+// Integer / select kernels: one opaque PTX instruction per step on runtime operands (the round-1
+// C++ bodies were folded by the compiler: IADD3 showed an impossible 2382 lanes/clk).  The SASS of
+// each loop body is checked with cuobjdump (tools/alu_peaks_sass.txt).
+#define AKERNEL(NAME, ASM)                                                               \
+    __global__ void NAME(unsigned *out, int seed) {                                     \
+        unsigned v[CH];                                                                 \
+        const unsigned a = (unsigned)seed * 2654435761u, b = (unsigned)seed ^ 0x9e3779b9u; \
+        _Pragma("unroll") for (int c = 0; c < CH; ++c) v[c] = threadIdx.x * 7919u + c;  \
+        _Pragma("unroll 16") for (int i = 0; i < ITER; ++i) {                           \
+            _Pragma("unroll") for (int c = 0; c < CH; ++c) asm volatile(ASM : "+r"(v[c]) : "r"(a), "r"(b)); \
+        }                                                                               \
+        unsigned s = v[0];                                                              \
+        _Pragma("unroll") for (int c = 1; c < CH; ++c) s ^= v[c];                       \
+        if (s == (unsigned)seed) out[threadIdx.x] = s;                                  \
+    }
+
 KERNEL(k_fadd, float, (float)(threadIdx.x + c), v[c] = __fadd_rn(v[c], 1.0001f * (c + 1)))
 KERNEL(k_ffma, float, (float)(threadIdx.x + c), v[c] = __fmaf_rn(v[c], 0.9999f, 1.0f))
-KERNEL(k_fmnmx, float, (float)(threadIdx.x + c), v[c] = fmaxf(fabsf(v[c] - 3.0f), (float)c))
-KERNEL(k_iadd3, int, (int)(threadIdx.x + c), v[c] = v[c] + c + seed)
-KERNEL(k_lop3, unsigned, (unsigned)(threadIdx.x + c), v[c] = (v[c] ^ 0x5a5a5a5au) & (v[c] | 0x0f0f0f0fu))
-KERNEL(k_vabsdiff4, unsigned, (unsigned)(threadIdx.x * 77 + c), v[c] = __vabsdiffu4(v[c], 0x01020304u * (c + 1)))
-KERNEL(k_dp4a, int, (int)(threadIdx.x + c), v[c] = __dp4a(v[c], 0x01010101, c))
+AKERNEL(k_fmnmx, "min.f32 %0, %0, %1;")
+AKERNEL(k_iadd3, "add.s32 %0, %0, %1;\n\tadd.s32 %0, %0, %2;")
+AKERNEL(k_lop3, "lop3.b32 %0, %0, %1, %2, 0x96;")
+AKERNEL(k_prmt, "prmt.b32 %0, %0, %1, %2;")
+AKERNEL(k_imnmx, "min.u32 %0, %0, %1;")
+AKERNEL(k_imad, "mad.lo.u32 %0, %0, %1, %2;")
+AKERNEL(k_vabsdiff4, "vabsdiff4.u32.u32.u32 %0, %0, %1, %2;")
+AKERNEL(k_dp4a, "dp4a.u32.u32 %0, %1, %2, %0;")
+AKERNEL(k_redux, "redux.sync.min.u32 %0, %0, 0xffffffff;")
 
 __global__ void k_fadd2(unsigned long long *out, int seed) {
     unsigned long long v[CH];
@@ -127,11 +147,15 @@ int main(int argc, char **argv) {
     const int n = p.multiProcessorCount;
     rate(k_fadd, 1, "FADD", n, clk, fb, js, false);
     rate(k_ffma, 1, "FFMA", n, clk, fb, js, false);
-    rate(k_fmnmx, 2, "FADD+FMNMX", n, clk, fb, js, false);
-    rate(k_iadd3, 1, "IADD3", n, clk, (int *)fb, js, false);
+    rate(k_fmnmx, 1, "FMNMX", n, clk, (unsigned *)fb, js, false);
+    rate(k_iadd3, 1, "IADD3", n, clk, (unsigned *)fb, js, false);
     rate(k_lop3, 1, "LOP3", n, clk, (unsigned *)fb, js, false);
+    rate(k_prmt, 1, "PRMT", n, clk, (unsigned *)fb, js, false);
+    rate(k_imnmx, 1, "IMNMX", n, clk, (unsigned *)fb, js, false);
+    rate(k_imad, 1, "IMAD", n, clk, (unsigned *)fb, js, false);
     rate(k_vabsdiff4, 1, "VABSDIFF4", n, clk, (unsigned *)fb, js, false);
-    rate(k_dp4a, 1, "IDP4A", n, clk, (int *)fb, js, false);
+    rate(k_dp4a, 1, "IDP4A", n, clk, (unsigned *)fb, js, false);
+    rate(k_redux, 1, "REDUX", n, clk, (unsigned *)fb, js, false);
     rate(k_fadd2, 1, "FADD2", n, clk, ub, js, false);
     rate(k_ffma2, 1, "FFMA2", n, clk, ub, js, false);
     rate(k_mix, 2, "FADD+LOP3", n, clk, fb, js, true);

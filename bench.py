@@ -257,6 +257,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     qs.qs_profile_reset()
+    qs.qs_certify_stats(reset=True)
     # The timed region: qs_profile's per-launch CUDA events are recorded on each launch's stream, so
     # in the refs and in_order modes (one stream) they time each kernel alone inside the timed region.
     qs.qs_profile_enable(True)
@@ -273,9 +274,11 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
     qs.qs_profile_enable(False)
+    rechecked = qs.qs_certify_stats(reset=True)
     ms = t0.elapsed_time(t1)
     prof = {k: qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS}
-    launches = sum(n for _, n in prof.values())
+    # kernels launched in the timed region: one per qs_profile scope, two for certify (scan + fix)
+    launches = sum(n for _, n in prof.values()) + prof["certify"][1]
     conc = None
     if cmp_mode:
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -353,6 +356,10 @@ def run_ours(args):
                           "l2": f"{args.frames} resident frames (~{args.frames * W * H * (6 if f32 else 3) / 1e6:.0f} MB vs "
                                 f"126 MB L2); consecutive steps use disjoint frames"},
                "roofline": roofline, "kernel_ms_per_step": kernel_ms, "gpu_launches": launches,
+               "certify": {"rechecked_per_step": rechecked / args.steps,
+                           "targets_per_step": round(3 * 0.75 * W * (band.y1 - band.y0)),
+                           "what": "float outputs whose argmin was not certified and were recomputed in the "
+                                   "definition's fp32 order (DESIGN.md 'Float certification')"} if f32 else None,
                "clocks": clk.summary(), "e2e": e2e, "compare": conc, "impl": "ours"}
         if args.variants:
             out["cc_variants_ms_per_frame"] = run_variants(qs, torch, dfr, roi, prm, fields, wss, W, H, K, S, f32)

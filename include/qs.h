@@ -201,7 +201,11 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
  * per-reference tail between launches).
  *
  *   refs        HOST array of n_refs DEVICE reference planes (same type, pitch)
- *   outs        HOST array of n_refs fields (each with its own planes / pitch)
+ *   outs        HOST array of n_refs fields (each with its own planes / pitch), or NULL
+ *               with a projection: "projection-only" -- the fields are not written, only
+ *               sum / cnt (the vectors never leave the chip except
+ *               as the projection overlay); needs K = 8 and no or the paper's FRMC offsets
+ *               (QS_EINVAL otherwise)
  *   proj        NULL, or the projection PR fused into the same launch: reference i's
  *               ACCEPTED entries project past_val[i] / past_mask[i] into sum / cnt
  *               exactly as qs_project(&outs[i], past_val[i], past_mask[i], ...) for

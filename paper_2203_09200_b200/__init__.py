@@ -254,19 +254,22 @@ def qs_me_search_refs(cur, cur_mask, refs, roi: qs_roi, params: qs_me_params, ou
     """qs_me_search for the pairs (cur, refs[i]) -> outs[i] of one frame in one launch per kernel.
 
     project = (past_vals, past_masks, sum, cnt): PR of every reference fused into the same launch
-    (as qs_project(outs[i], past_vals[i], past_masks[i], roi, sum, cnt) for each i)."""
+    (as qs_project(outs[i], past_vals[i], past_masks[i], roi, sum, cnt) for each i).
+    outs = None with project: projection-only (no field planes written)."""
     if _pitch_bytes(cur) != _pitch_bytes(cur_mask):
         raise ValueError("cur and cur_mask must share one pitch")
     n = len(refs)
-    if len(outs) != n:
+    if outs is not None and len(outs) != n:
         raise ValueError("refs and outs differ in length")
+    if outs is None and project is None:
+        raise ValueError("outs=None (projection-only) needs project=")
     pitches = {_pitch_bytes(r) for r in refs}
     if len(pitches) > 1:
         raise ValueError("reference planes must share one pitch")
     if ws is None:
         ws = workspace(roi, params, cur.device, n)
     rp = (C.c_void_p * max(n, 1))(*[r.data_ptr() for r in refs])
-    fc = (qs_field * max(n, 1))(*[o.c() for o in outs])
+    fc = (qs_field * max(n, 1))(*[o.c() for o in outs]) if outs is not None else None
     pj = None
     if project is not None:
         pvs, pms, acc_sum, acc_cnt = project
@@ -284,7 +287,8 @@ def qs_me_search_refs(cur, cur_mask, refs, roi: qs_roi, params: qs_me_params, ou
         pj._keep = (pva, pma)
     _check(lib().qs_me_search_refs(_ptr(cur), _ptr(cur_mask), _pitch_bytes(cur), n, C.cast(rp, C.c_void_p),
                                    pitches.pop() if pitches else 16, C.byref(roi), C.byref(params),
-                                   C.byref(fuse) if fuse is not None else None, C.cast(fc, C.c_void_p),
+                                   C.byref(fuse) if fuse is not None else None,
+                                   C.cast(fc, C.c_void_p) if fc is not None else None,
                                    C.byref(pj) if pj is not None else None,
                                    _ptr(eval_count), _ptr(ws), ws.numel(), _stream(stream)))
 

@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
     };
     // Only the roi's rows [y0, y1) are written: the NNC halo rows were decoded for the median only
     // (a neighbouring band's call owns them; writing them would race with it on a shared field).
-    if (own && checked_row) {
+    if (own && checked_row && g.write_field) {
         const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f_p[zr].pitch + gx;
         const bool has = st >= kCandidate;
         g.f_p[zr].alpha[fi] = has ? (int8_t)a : (int8_t)0;
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
             S.rej[o] = 1;
     }
     __syncthreads();
-    if (own && checked_row) {
+    if (own && checked_row && g.write_field) {
         const bool checked = checked_row && (st == kCandidate || st == kAccepted);
         const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f_p[zr].pitch + gx;
         g.f_p[zr].status[fi] = checked ? (S.rej[tid] ? kRejected : kAccepted) : st;

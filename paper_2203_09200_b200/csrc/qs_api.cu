@@ -228,11 +228,41 @@ size_t rme_keys_bytes(const Roi &r, int S) {
 // Workspace slot: the 64-bit key plane, then (float references) the 32-bit second plane of the
 // certified argmin.  qs_me_search_refs lays out the key planes of
 // its n slots first and their second planes after them.
-// qs_me_search with K != 8 and NNC also keeps a scratch field (8 B per pixel, like the keys) for the
-// ME rows [y0-2, y1+2): NNC reads the halo rows there and only the roi's rows reach the caller's field.
+// Workspace layout of one call over n slots (key planes of kb bytes each): the n key planes; for
+// float references their n second planes, the certify list (one 4-byte entry per 16 outputs; a
+// full list only slows the certify kernel down) and its counter; then, for qs_me_search with K != 8
+// and NNC, a scratch field (8 B per pixel, like the keys) for the ME rows [y0-2, y1+2): NNC reads
+// the halo rows there and only the roi's rows reach the caller's field.
+struct WsLayout {
+    size_t keys, s2, list, count, scratch, total;
+    size_t kba, s2a;
+    int cap;
+};
+WsLayout ws_layout(size_t kb, int n, bool f32, bool scratch) {
+    WsLayout L{};
+    L.kba = al256(kb);
+    L.s2a = al256(kb / 2);
+    size_t off = 0;
+    L.keys = off;
+    off += n * L.kba;
+    L.s2 = off;
+    L.cap = 0;
+    if (f32) {
+        off += n * L.s2a;
+        L.cap = (int)std::max<size_t>(32, n * (kb / 8) / 16);
+        L.list = off;
+        off += al256(4 * (size_t)L.cap);
+        L.count = off;
+        off += 256;
+    }
+    L.scratch = off;
+    if (scratch) off += L.kba;
+    L.total = off;
+    return L;
+}
 size_t ws_slot_bytes(const Roi &r, int S) {
     const size_t me = me_keys_bytes(r), rme = rme_keys_bytes(r, S);
-    return std::max(2 * al256(me) + al256(me / 2), al256(rme) + al256(rme / 2));
+    return std::max(ws_layout(me, 1, true, true).total, ws_layout(rme, 1, true, false).total);
 }
 
 BoxArgs box_args(const Roi &r, const uint8_t *cur, const uint8_t *mask, int64_t cur_pitch, const void *ref,
@@ -266,13 +296,15 @@ int check_offsets(const int8_t *offs, int n, int S) {
 }
 
 // Certificate + exact recompute of the float argmin (certify.cu) over the keys of a box launch.
-int run_certify(const BoxArgs &a, int K, bool ssd, bool reverse, const CandTables *t, cudaStream_t s) {
+int run_certify(const BoxArgs &a, int K, bool ssd, bool reverse, const CandTables *t, char *ws, const WsLayout &L,
+                cudaStream_t s) {
     CertifyArgs c{};
     c.cur = a.cur;
     c.mask = a.mask;
     c.ref = a.ref;
     c.ssd = ssd;
     c.K = K;
+    c.S = a.S;
     c.W = a.W;
     c.H = a.H;
     c.buf_y0 = a.buf_y0;
@@ -292,7 +324,9 @@ int run_certify(const BoxArgs &a, int K, bool ssd, bool reverse, const CandTable
     }
     c.canon = t->canon;
     c.n_cand = t->n;
-    c.rechecked = rechecked_counter();
+    c.list = reinterpret_cast<unsigned *>(ws + L.list);
+    c.list_count = reinterpret_cast<unsigned *>(ws + L.count);
+    c.list_cap = L.cap;
     cudaError_t e;
     {
         ProfScope ps(P_CERTIFY, s);
@@ -372,8 +406,9 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
         return rc;
     const bool f32 = p->ref_type == QS_REF_F32;
     const size_t kb = me_keys_bytes(r);
-    const bool scratch = K != 8 && nnc;   // finalize + NNC through a scratch field (ws_slot_bytes)
-    const size_t need = scratch ? 2 * al256(kb) + al256(kb / 2) : f32 ? al256(kb) + al256(kb / 2) : kb;
+    const bool scratch = K != 8 && nnc;   // finalize + NNC through a scratch field (ws_layout)
+    const WsLayout L = ws_layout(kb, 1, f32, scratch);
+    const size_t need = L.total;
     if (!workspace || !aligned16(workspace) || workspace_bytes < need)
         return fail(QS_EDIM, "workspace: need %zu bytes (16-byte aligned), got %zu", need, workspace_bytes);
     const char *terr = nullptr;
@@ -383,7 +418,8 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     if (r.y1 <= r.y0 || hi <= lo) return QS_OK;   // empty roi: nothing is written
 
     auto *keys = static_cast<unsigned long long *>(workspace);
-    unsigned *s2 = f32 ? reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + al256(kb)) : nullptr;
+    char *wsc = static_cast<char *>(workspace);
+    unsigned *s2 = f32 ? reinterpret_cast<unsigned *>(wsc + L.s2) : nullptr;
     cudaError_t e = cudaMemsetAsync(keys, 0xff, sizeof(unsigned long long) * (size_t)(hi - lo) * r.W, s);
     if (e == cudaSuccess && f32) e = cudaMemsetAsync(s2, 0xff, sizeof(unsigned) * (size_t)(hi - lo) * r.W, s);
     if (e != cudaSuccess) return cuda_fail(e, "memset keys");
@@ -402,7 +438,7 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
         e = launch_box(a, K, p->err == QS_SSD, false, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "me_box launch");
-    if (f32 && (rc = run_certify(a, K, p->err == QS_SSD, false, t, s))) return rc;
+    if (f32 && (rc = run_certify(a, K, p->err == QS_SSD, false, t, wsc, L, s))) return rc;
 
     if (K == 8) {
         // Fused epilogue: finalize + NNC + FRMC (the paper's offsets, in any order) in one launch.
@@ -427,6 +463,7 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
         g.key_pitch = r.W;
         g.canon = t->canon;
         g.f = view(out);
+        g.write_field = 1;
         g.nnc = nnc ? fuse->nnc : 0;
         g.nnc_threshold = nnc ? fuse->nnc_threshold : 0;
         g.frmc = paper;
@@ -465,7 +502,7 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     // Without NNC the ME rows are the roi's: finalize straight into the caller's field.  With NNC the
     // rows [lo, hi) go to a scratch field (the halo rows belong to the neighbouring bands' calls), NNC
     // decides [y0, y1) there and those rows are copied out.
-    char *sc = static_cast<char *>(workspace) + al256(kb) + al256(kb / 2);
+    char *sc = wsc + L.scratch;
     const int64_t sn = (int64_t)(hi - lo) * r.W;
     qs_field tmp{reinterpret_cast<int8_t *>(sc), reinterpret_cast<int8_t *>(sc + sn), sc + 4 * sn,
                  reinterpret_cast<uint8_t *>(sc + 2 * sn), reinterpret_cast<uint8_t *>(sc + 3 * sn), r.W};
@@ -519,7 +556,8 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
     Roi r;
     int rc;
     if (n_refs < 0) return fail(QS_EINVAL, "n_refs=%d", n_refs);
-    if (n_refs > 0 && (!refs || !outs)) return fail(QS_EINVAL, "refs / outs is NULL");
+    if (n_refs > 0 && !refs) return fail(QS_EINVAL, "refs is NULL");
+    if (n_refs > 0 && !outs && !proj) return fail(QS_EINVAL, "outs is NULL (allowed only with a projection)");
     if ((rc = check_roi(roi, &r)) || (rc = check_params(p))) return rc;
     if (proj && n_refs > 0) {
         if (!proj->past_val || !proj->past_mask || !proj->sum || !proj->cnt)
@@ -545,6 +583,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
     const bool paper = frmc && is_paper_offsets(fuse->offsets, fuse->n_offsets);
     // The single-launch path covers the fused K = 8 epilogue; everything else runs slot by slot.
     if (p->K_h != 8 || (frmc && !paper)) {
+        if (!outs) return fail(QS_EINVAL, "outs is NULL: projection-only needs K = 8 and the paper's FRMC offsets");
         for (int i = 0; i < n_refs; ++i) {
             if ((rc = qs_me_search(cur, cur_mask, cur_pitch, refs[i], ref_pitch, roi, p, fuse, &outs[i], eval_count,
                                    ws + slot * i, slot, stream)))
@@ -562,7 +601,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
             return rc;
         for (int i = 0; i < n; ++i)
             if ((rc = check_plane(refs[i0 + i], ref_pitch, (int64_t)r.W * esz, "ref")) ||
-                (rc = check_field(&outs[i0 + i], r.W, true)))
+                (outs && (rc = check_field(&outs[i0 + i], r.W, true))))
                 return rc;
         if (nnc && fuse->nnc_threshold < 0) return fail(QS_EINVAL, "nnc_threshold < 0");
         if (fuse && (fuse->nnc < 0 || fuse->nnc > QS_NNC_PAIRS)) return fail(QS_EINVAL, "nnc mode %d", fuse->nnc);
@@ -576,13 +615,15 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
         if (!t) return fail(QS_ECUDA, "%s", terr);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         if (r.y1 <= r.y0 || hi <= lo) return QS_OK;
-        const size_t kb = me_keys_bytes(r), kba = al256(kb), s2a = al256(kb / 2);
+        const size_t kb = me_keys_bytes(r);
         const bool f32 = p->ref_type == QS_REF_F32;
+        const WsLayout L = ws_layout(kb, n, f32, false);   // <= n * slot bytes
+        const size_t kba = L.kba, s2a = L.s2a;
         char *wg = ws + slot * i0;
         // The group's n slots: key planes at wg + i * kba, then (float) second planes at
-        // wg + n * kba + i * s2a (within the n * slot bytes of the group); one memset per span.
+        // wg + L.s2 + i * s2a; one memset per span.
         cudaError_t e = cudaMemsetAsync(wg, 0xff, kba * (n - 1) + kb, s);
-        if (e == cudaSuccess && f32) e = cudaMemsetAsync(wg + n * kba, 0xff, s2a * (n - 1) + kb / 2, s);
+        if (e == cudaSuccess && f32) e = cudaMemsetAsync(wg + L.s2, 0xff, s2a * (n - 1) + kb / 2, s);
         if (e != cudaSuccess) return cuda_fail(e, "memset keys");
         BoxArgs a = box_args(r, cur, cur_mask, cur_pitch, refs[i0], ref_pitch, p, t);
         a.oy0 = lo;
@@ -597,7 +638,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
         for (int i = 0; i < n; ++i) {
             a.ref_p[i] = static_cast<const uint8_t *>(refs[i0 + i]);
             a.keys_p[i] = reinterpret_cast<unsigned long long *>(wg + kba * i);
-            a.s2_p[i] = f32 ? reinterpret_cast<unsigned *>(wg + n * kba + s2a * i) : nullptr;
+            a.s2_p[i] = f32 ? reinterpret_cast<unsigned *>(wg + L.s2 + s2a * i) : nullptr;
         }
         a.s2 = a.s2_p[0];
         {
@@ -605,7 +646,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
             e = launch_box(a, 8, p->err == QS_SSD, false, s);
         }
         if (e != cudaSuccess) return cuda_fail(e, "me_box launch");
-        if (f32 && (rc = run_certify(a, 8, p->err == QS_SSD, false, t, s))) return rc;
+        if (f32 && (rc = run_certify(a, 8, p->err == QS_SSD, false, t, wg, L, s))) return rc;
         EpiArgs g{};
         g.cur = a.cur;
         g.mask = a.mask;
@@ -625,7 +666,8 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
         g.keys = a.keys;
         g.key_pitch = r.W;
         g.canon = t->canon;
-        g.f = view(&outs[i0]);
+        g.f = outs ? view(&outs[i0]) : FieldView{};
+        g.write_field = outs != nullptr;
         g.nnc = nnc ? fuse->nnc : 0;
         g.nnc_threshold = nnc ? fuse->nnc_threshold : 0;
         g.frmc = paper;
@@ -636,7 +678,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
         for (int i = 0; i < n; ++i) {
             g.ref_p[i] = a.ref_p[i];
             g.keys_p[i] = a.keys_p[i];
-            g.f_p[i] = view(&outs[i0 + i]);
+            g.f_p[i] = outs ? view(&outs[i0 + i]) : FieldView{};
         }
         if (proj) {
             g.proj = 1;
@@ -683,12 +725,14 @@ int qs_reverse_check(int32_t mode, const uint8_t *cur, const uint8_t *cur_mask, 
     if ((rc = need_rows(r, r.y0 - 2 * S - KL, r.y1 + 2 * S + KR, "RME inputs"))) return rc;
     const bool f32 = p->ref_type == QS_REF_F32;
     const size_t kb = rme_keys_bytes(r, S);
-    const size_t need = f32 ? al256(kb) + al256(kb / 2) : kb;
+    const WsLayout L = ws_layout(kb, 1, f32, false);
+    const size_t need = L.total;
     if (!workspace || !aligned16(workspace) || workspace_bytes < need)
         return fail(QS_EDIM, "workspace: need %zu bytes (16-byte aligned), got %zu", need, workspace_bytes);
     if (r.y1 <= r.y0) return QS_OK;
     auto *keys = static_cast<unsigned long long *>(workspace);
-    unsigned *s2 = f32 ? reinterpret_cast<unsigned *>(static_cast<char *>(workspace) + al256(kb)) : nullptr;
+    char *wsc = static_cast<char *>(workspace);
+    unsigned *s2 = f32 ? reinterpret_cast<unsigned *>(wsc + L.s2) : nullptr;
     cudaError_t e = cudaMemsetAsync(keys, 0xff, kb, s);
     if (e == cudaSuccess && f32) e = cudaMemsetAsync(s2, 0xff, kb / 2, s);
     if (e != cudaSuccess) return cuda_fail(e, "memset keys");
@@ -707,7 +751,7 @@ int qs_reverse_check(int32_t mode, const uint8_t *cur, const uint8_t *cur_mask, 
         e = launch_box(a, K, p->err == QS_SSD, true, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "rme box launch");
-    if (f32 && (rc = run_certify(a, K, p->err == QS_SSD, true, t, s))) return rc;
+    if (f32 && (rc = run_certify(a, K, p->err == QS_SSD, true, t, wsc, L, s))) return rc;
     RmeDecideArgs d{};
     d.W = r.W;
     d.H = r.H;

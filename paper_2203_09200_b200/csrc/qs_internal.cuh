@@ -97,7 +97,7 @@ constexpr float kAdmissibleMax = 1.0e38f;
 // Forward / reverse certification and exact recompute of uncertain outputs (certify.cu).
 struct CertifyArgs {
     Plane cur, mask, ref;
-    int ssd, K;
+    int ssd, K, S;
     int W, H, buf_y0, buf_rows, min_support;
     int oy0, oy1, ox0, ox1;          // key domain (frame coordinates)
     int64_t key_pitch;
@@ -108,7 +108,9 @@ struct CertifyArgs {
     const unsigned *s2_p[kMaxRefs];
     const int32_t *canon;
     int n_cand;
-    unsigned long long *rechecked;   // nullable device counter: outputs recomputed exactly
+    unsigned *list;                  // workspace: uncertain outputs (slot << 30 | y - oy0 << 16 | x - ox0)
+    unsigned *list_count;            // workspace: entries appended (zeroed by launch_certify)
+    int list_cap;
 };
 cudaError_t launch_certify(const CertifyArgs &a, cudaStream_t s);
 unsigned long long *rechecked_counter();   // current device's counter (nullptr on failure)
@@ -175,6 +177,7 @@ struct EpiArgs {
     const int32_t *canon;
     FieldView f;
     int nnc, nnc_threshold, frmc;
+    int write_field;                 // 0: projection-only (qs_me_search_refs with outs == NULL)
     int8_t dys[8];                   // FRMC delta_y order (a permutation of the paper's offsets)
     unsigned long long *evals;
     int n_ref;                       // slots per launch (grid z); 0 -> 1 with slot 0 = (ref, keys, f)

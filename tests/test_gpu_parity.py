@@ -811,3 +811,36 @@ def test_adjacent_rois_share_one_field(K, f32):
         g["err"] = g["err"].view(np.uint32)
     o, _ = oracle.pair_chain(inp, K=K, S=S, check="nnc_frmc", threads=_THREADS)
     assert_field_equal(g, o, what=f"adjacent rois K={K} f32={f32}")
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_projection_only_mode(cfg):
+    """qs_me_search_refs with outs = NULL: only sum / cnt are written, and
+    they equal the oracle's chain + PR over the three references."""
+    c = synth.CONFIGS[cfg]
+    seq = synth.make_sequence(cfg, w=256, h=160)
+    t, S = 6, min(c.S, 16)
+    inps = [synth.pair_inputs(seq, t, d) for d in (1, 2, 3)]
+    H, W = inps[0]["cur"].shape
+    cur = qs.to_plane(inps[0]["cur"], DEV_)
+    msk = qs.to_plane(inps[0]["cur_mask"], DEV_)
+    refs = [qs.to_plane(i["ref"], DEV_) for i in inps]
+    pvs = [qs.to_plane(i["past_val"], DEV_) for i in inps]
+    pms = [qs.to_plane(i["past_mask"], DEV_) for i in inps]
+    s, cn = qs.alloc_acc(H, W, DEV_)
+    ev = torch.zeros(1, dtype=torch.int64, device=DEV_)
+    qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H), qs.make_params(K=8, S=S, ref_f32=c.ref_f32), None,
+                         fuse=qs.make_checks(), project=(pvs, pms, s, cn), eval_count=ev)
+    torch.cuda.synchronize()
+    osum = np.zeros((H, W), np.uint32)
+    ocnt = np.zeros((H, W), np.uint8)
+    oev = 0
+    for inp in inps:
+        o, e = oracle.pair_chain(inp, K=8, S=S, check="nnc_frmc", threads=_THREADS)
+        osum, ocnt = oracle.project(o, inp["past_val"], inp["past_mask"], osum, ocnt)
+        oev += e
+    assert np.array_equal(s.cpu().numpy().view(np.uint32), osum) and np.array_equal(cn.cpu().numpy(), ocnt)
+    assert int(ev.item()) == oev
+    with pytest.raises(qs.QsError):   # projection-only needs the fused K = 8 path
+        qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H), qs.make_params(K=7, S=S, ref_f32=c.ref_f32), None,
+                             fuse=qs.make_checks(), project=(pvs, pms, s, cn))

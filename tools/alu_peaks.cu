@@ -24,7 +24,9 @@ constexpr int CH = 8;
 
 // Integer / select kernels: one opaque PTX instruction per step on runtime operands (the round-1
 // C++ bodies were folded by the compiler: IADD3 showed an impossible 2382 lanes/clk).  The SASS of
-// each loop body is checked with cuobjdump (tools/alu_peaks_sass.txt).
+// each loop body is checked with cuobjdump (tools/alu_peaks_sass.txt): ptxas merges two dependent
+// min.f32 / min.u32 into one 3-input FMNMX3 / VIMNMX3 (rate counted per SASS instruction, 0.5 per
+// step), and splits dependent add.s32 between IADD3 (ALU pipe) and IMAD (FMA-heavy pipe).
 #define AKERNEL(NAME, ASM)                                                               \
     __global__ void NAME(unsigned *out, int seed) {                                     \
         unsigned v[CH];                                                                 \
@@ -111,7 +113,7 @@ __global__ void k_mix(float *out, int seed) {
 }
 
 template <typename K, typename T>
-double rate(K kern, int instr_per_step, const char *name, int sm_count, double clk_hz, T *buf, FILE *js, bool last) {
+double rate(K kern, double instr_per_step, const char *name, int sm_count, double clk_hz, T *buf, FILE *js, bool last) {
     const int threads = 256, blocks = sm_count * 8;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -147,11 +149,11 @@ int main(int argc, char **argv) {
     const int n = p.multiProcessorCount;
     rate(k_fadd, 1, "FADD", n, clk, fb, js, false);
     rate(k_ffma, 1, "FFMA", n, clk, fb, js, false);
-    rate(k_fmnmx, 1, "FMNMX", n, clk, (unsigned *)fb, js, false);
-    rate(k_iadd3, 1, "IADD3", n, clk, (unsigned *)fb, js, false);
+    rate(k_fmnmx, 0.5, "FMNMX3", n, clk, (unsigned *)fb, js, false);
+    rate(k_iadd3, 2, "IADD3+IMAD(add)", n, clk, (unsigned *)fb, js, false);
     rate(k_lop3, 1, "LOP3", n, clk, (unsigned *)fb, js, false);
     rate(k_prmt, 1, "PRMT", n, clk, (unsigned *)fb, js, false);
-    rate(k_imnmx, 1, "IMNMX", n, clk, (unsigned *)fb, js, false);
+    rate(k_imnmx, 0.5, "VIMNMX3", n, clk, (unsigned *)fb, js, false);
     rate(k_imad, 1, "IMAD", n, clk, (unsigned *)fb, js, false);
     rate(k_vabsdiff4, 1, "VABSDIFF4", n, clk, (unsigned *)fb, js, false);
     rate(k_dp4a, 1, "IDP4A", n, clk, (unsigned *)fb, js, false);

@@ -6,7 +6,8 @@ import csv
 import json
 import sys
 
-OURS = ("box_kernel", "epilogue_kernel", "project_kernel", "finalize_kernel", "nnc_kernel", "revgrid", "rme_decide")
+OURS = ("box_kernel", "epilogue_kernel", "certify_scan_kernel", "certify_fix_kernel", "project_kernel", "finalize_kernel",
+        "nnc_kernel", "revgrid", "rme_decide")
 
 
 def main():

@@ -63,6 +63,9 @@ def parse():
                     help="how a step runs its three (frame, reference) pairs: refs = one qs_me_search_refs call "
                          "(one launch per kernel for the three references; default), in_order = three "
                          "qs_me_search calls on one stream, streams = three calls on three streams")
+    ap.add_argument("--fields", action="store_true",
+                    help="refs mode: also write the three motion fields (default: projection-only, SURVEY.md 8(f) "
+                         "NEXT-1 -- the vectors stay on chip and only sum / cnt are written)")
     ap.add_argument("--no-compare", action="store_true",
                     help="skip the extra timed loop that runs the same steps as three in-order qs_me_search calls")
     return ap.parse_args()
@@ -218,8 +221,8 @@ def run_ours(args):
         if mode == "refs":       # ME + checks of the three pairs: one launch per kernel
             fr = dfr[t]
             past = [dfr[t - d] for d in (1, 2, 3)]
-            qs.qs_me_search_refs(fr["cur"], fr["mask"], [x["ref"] for x in past], roi, prm, fields,
-                                 fuse=checks, eval_count=evals, ws=ws3,
+            qs.qs_me_search_refs(fr["cur"], fr["mask"], [x["ref"] for x in past], roi, prm,
+                                 fields if args.fields else None, fuse=checks, eval_count=evals, ws=ws3,
                                  project=([x["cur"] for x in past], [x["mask"] for x in past], acc_s, acc_c))
             return
         if mode == "in_order":
@@ -350,7 +353,9 @@ def run_ours(args):
                           "parallelism": (f"sequences{world}" if args.sequences else f"rowband{world}") if world > 1
                           else "single",
                           "pairs": {"refs": "one qs_me_search_refs call per step (ME, checks and PR of the "
-                                            "three references: one me_box and one epilogue launch)",
+                                            "three references: one me_box, one epilogue launch (+ certify for "
+                                            "float references)); " + ("fields written" if args.fields else
+                                            "projection-only: only sum / cnt written (NEXT-1)"),
                                     "in_order": "three qs_me_search calls in order on one stream",
                                     "streams": "three qs_me_search calls on three streams"}[args.pairs],
                           "l2": f"{args.frames} resident frames (~{args.frames * W * H * (6 if f32 else 3) / 1e6:.0f} MB vs "
@@ -430,7 +435,7 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
             acc_c.zero_()
             if args.pairs == "refs":
                 qs.qs_me_search_refs(slots[0]["cur"], slots[0]["mask"], [slots[d]["ref"] for d in (1, 2, 3)], roi,
-                                     prm, fields, fuse=checks, ws=ws3,
+                                     prm, fields if args.fields else None, fuse=checks, ws=ws3,
                                      project=([slots[d]["cur"] for d in (1, 2, 3)],
                                               [slots[d]["mask"] for d in (1, 2, 3)], acc_s, acc_c))
             elif args.pairs == "streams":

@@ -22,7 +22,11 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqs.so")
+# QS_LIBQS selects another build of the same sources (test infrastructure: libqs_checked.so, the
+# bounds-checked build); the default is the product library.
+LIB_PATH = os.environ.get("QS_LIBQS") or os.path.join(_HERE, "libqs.so")
+if not os.path.isabs(LIB_PATH):
+    LIB_PATH = os.path.join(_HERE, LIB_PATH)
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "qs.h")
 
 # Return codes, statuses, enums (include/qs.h).

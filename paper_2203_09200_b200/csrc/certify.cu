@@ -219,7 +219,10 @@ __global__ void __launch_bounds__(256) certify_fix_kernel(const CertifyArgs a) {
             const int off = (int)(int8_t)(pk & 0xff) * span + (int)(int8_t)((pk >> 8) & 0xff);
             float e = 0.f;
             int n = 0;
-            for (int i = 0; i < m; ++i) add_term(cval[i], win[cpos[i] + off], a.ssd, e, n);
+            for (int i = 0; i < m; ++i) {
+                QS_DCHECK(cpos[i] + off >= 0 && cpos[i] + off < span * span);
+                add_term(cval[i], win[cpos[i] + off], a.ssd, e, n);
+            }
             if (n < a.min_support) continue;
             best = kmin(best, ((unsigned long long)__float_as_uint(__fdiv_rn(e, (float)n)) << 32) | (unsigned)rk);
         }

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
             const bool measured = (tile::mask_bits(R, cr, cc) & 1u) != 0;
             if (!measured) {
                 st0 = kInvalid;
+                QS_DCHECK(gy >= g.lo && gy < g.hi && gx < g.key_pitch);
                 const unsigned long long key = keys[(int64_t)(gy - g.lo) * g.key_pitch + gx];
                 if (key != ~0ull) {
                     const int pk = __ldg(g.canon + (int)(key & 0xffffffffu));
@@ -171,6 +172,8 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
         const int rrow = (gy + a - KL) - R.ry0, rcol = (gx + b - KL) - R.rx0;
 #pragma unroll 1
         for (int oy = 0; oy < kFK; ++oy) {
+            QS_DCHECK(crow + oy >= 0 && crow + oy < R.CR && ccol >= 0 && ccol + kFK <= R.cpitch);
+            QS_DCHECK(rrow + oy >= 0 && rrow + oy < R.RR && rcol >= 0 && rcol + kFK <= R.rpitch);
             const float *cp = R.Cs + (crow + oy) * R.cpitch + ccol;
             const float *rp = R.Rs + (rrow + oy) * R.rpitch + rcol;
 #pragma unroll
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
     // Only the roi's rows [y0, y1) are written: the NNC halo rows were decoded for the median only
     // (a neighbouring band's call owns them; writing them would race with it on a shared field).
     if (own && checked_row && g.write_field) {
+        QS_DCHECK(gy >= g.buf_y0 && gy < g.buf_y0 + g.buf_rows && gx < g.f_p[zr].pitch);
         const int64_t fi = (int64_t)(gy - g.buf_y0) * g.f_p[zr].pitch + gx;
         const bool has = st >= kCandidate;
         g.f_p[zr].alpha[fi] = has ? (int8_t)a : (int8_t)0;

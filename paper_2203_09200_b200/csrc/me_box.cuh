@@ -76,6 +76,9 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // and the second plane: the 64-bit atomicMin orders (v1, rank) across chunks; whoever does not end
 // up the winner -- this contribution when it loses, the displaced key when it wins -- pushes its
 // value into s2, so s2 ends as the smallest value of every candidate but the final winner.
+__device__ __forceinline__ void check_key(const BoxArgs &a, int py, int px) {
+    QS_DCHECK(py >= a.oy0 && py < a.oy1 && px >= a.ox0 && px - a.ox0 < a.key_pitch);
+}
 __device__ __forceinline__ void merge_f32(unsigned long long *kp, unsigned *sp, unsigned v1, int rank, unsigned v2) {
     const unsigned long long key = ((unsigned long long)v1 << 32) | (unsigned)rank;
     const unsigned long long old = atomicMin(kp, key);
@@ -224,6 +227,8 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
         const bool clipfree = !REV && tile_clip_free<K>(a, px0, py0, al, bt);   // uniform
         if (actA) {
             const float *brow = Bw + (ya + al - alo) * bpitch + xa0 + bt + a.S;
+            QS_DCHECK(ya + al - alo >= 0 && ya + al - alo < nrow_b && xa0 + bt + a.S >= 0 &&
+                      xa0 + bt + a.S + G::NA <= ncol_b);
             float d[G::NA];
             float nv[CNT ? G::NA : 1];
 #pragma unroll
@@ -310,6 +315,7 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
         if constexpr (!EXACT) {
             // float: keyed winner (e for n constant, else e * rcp(n)) and second, certified later
             if (!(be[i] < kAdmissibleMax) || py >= a.oy1 || px >= a.ox1) continue;
+            check_key(a, py, px);
             const int64_t o = (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0);
             const int rank = clist[__float_as_uint(be[i]) & kKeyBits] >> 16;
             merge_f32(a.keys_p[ref_slot(a)] + o, a.s2_p[ref_slot(a)] + o, fkey_val(be[i]), rank, fkey_val2(bn[i]));
@@ -326,6 +332,7 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
             hi = (unsigned long long)floor((double)be[i] * 8192.0 / (double)bn[i]);
         }
         const unsigned long long key = (hi << 32) | (unsigned)br[i];
+        check_key(a, py, px);
         atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
     }
 }
@@ -365,6 +372,7 @@ constexpr int kQBarI = 64 + 128;        // threads on an interior FULL / EMPTY b
 constexpr int kQSeg = kQBY / 2;         // 14 output block rows per consumer lane (2 row halves x C/D planes)
 constexpr int kQWinRows = 2 * kQHR;     // 64 pixel rows of blocks per tile (+ alpha range)
 constexpr int kQWinCols = 2 * (4 * kQRun + 4);  // 72 pixel columns (blocks -2 .. 33)
+static_assert(kQWinRows == kQWinRowsHost && kQWinCols == kQWinColsHost, "host copies of the window size");
 
 // Named barriers with immediate ids (1..4), so ptxas reserves only the ones used.
 template <int ID, int CNT = kNT>
@@ -498,8 +506,11 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     // Reference window split by row parity: row y at plane (y & 1), plane row y >> 1.  Row pitch
     // bpitch = 2 x odd and plane pitch = 0 mod 32 words: a warp's 32 gathers (one block row per lane,
     // the block's row parity choosing the plane) fall into distinct banks except lanes 16 apart.
-    const int bpitch = quad_pitch(ncol_b);
-    const int bplane = quad_plane(nrow_b, ncol_b);
+    // With TMA (float references) the planes hold the descriptor's box: tma_rows rows of tma_cols
+    // floats (a multiple of 4: TMA rows are 16-byte multiples, which costs the conflict-light pitch).
+    const bool tma = a.tma != 0;
+    const int bpitch = tma ? a.tma_cols : quad_pitch(ncol_b);
+    const int bplane = tma ? ((a.tma_rows * a.tma_cols + 31) & ~31) : quad_plane(nrow_b, ncol_b);
     float *Bw = smem;
     f2_t *Hp = reinterpret_cast<f2_t *>(smem + 2 * bplane);   // [kQStages][kQPlanes][kQHR][kQHP]
     int *clist = reinterpret_cast<int *>(Hp + kQStages * kQPlanes * kQHR * kQHP);   // the chunk's candidates
@@ -510,7 +521,34 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     // Stage the chunk's reference window (rows py0-4+alo .., cols px0-4-S ..) and candidate list.
     const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    {
+    __shared__ __align__(8) unsigned long long tma_bar;
+    if (tma) {
+        // Two TMA box loads (row-parity planes p = 0, 1: window rows by0 + p, by0 + p + 2, ...),
+        // completion counted on one mbarrier; the hardware fills NaN outside the frame and buffer.
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&tma_bar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const unsigned bytes = 2u * (unsigned)(a.tma_rows * a.tma_cols) * 4u;
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            const CUtensorMap *tm = &a.tmap[ref_slot(a)];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const int b = by0 + p - a.buf_y0;   // buffer row of window row p
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(Bw + p * bplane);
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                    ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tm)), "r"(bx0), "r"(b & 1), "r"(b >> 1), "r"(bar)
+                    : "memory");
+            }
+        }
+        __syncthreads();
+        asm volatile(
+            "{\n\t.reg .pred P;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared.b64 P, [%0], 0;\n\t"
+            "@!P bra WAIT_%=;\n\t}" ::"r"(bar) : "memory");
+    } else {
         // One window row per warp iteration, lanes along the row (coalesced, no index division).
         // float references: in-frame values go global -> shared by cp.async (no register round
         // trip, many copies in flight); everything else (uint8 conversion, NaN outside the frame or
@@ -615,7 +653,11 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                     const char *bwc = reinterpret_cast<const char *>(
                         Bw + (((int)(int8_t)(pk & 0xff) - alo) >> 1) * bpitch + (int)(int8_t)((pk >> 8) & 0xff));
 #pragma unroll
-                    for (int kk = 0; kk < kQGI; ++kk) rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
+                    for (int kk = 0; kk < kQGI; ++kk) {
+                        QS_DCHECK(bwc + ad[kk] >= reinterpret_cast<const char *>(Bw) &&
+                                  bwc + ad[kk] + 4 <= reinterpret_cast<const char *>(Bw + 2 * bplane));
+                        rv[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
+                    }
                 };
                 for (int k = P; k < nA; k += 2) {
                     gather(k);
@@ -704,6 +746,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                     const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
                     if constexpr (FK) {
                         if (!(be[r][c] < kAdmissibleMax) || py >= a.oy1 || px >= a.ox1) continue;
+                        check_key(a, py, px);
                         const int64_t o = (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0);
                         merge_f32(a.keys_p[ref_slot(a)] + o, a.s2_p[ref_slot(a)] + o, fkey_val(be[r][c]),
                                   clist[__float_as_uint(be[r][c]) & kKeyBits] >> 16, fkey_val2(m2[r][c]));
@@ -717,7 +760,8 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                         if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
                         const unsigned long long key =
                             ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
-                        atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+                        check_key(a, py, px);
+        atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
                     }
                 }
         }
@@ -761,7 +805,11 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             const char *bwc = reinterpret_cast<const char *>(Bw + (((int)(int8_t)(pk & 0xff) - alo) >> 1) * bpitch +
                                                              (int)(int8_t)((pk >> 8) & 0xff));
 #pragma unroll
-            for (int kk = 0; kk < kQG; ++kk) dst[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
+            for (int kk = 0; kk < kQG; ++kk) {
+                QS_DCHECK(bwc + ad[kk] >= reinterpret_cast<const char *>(Bw) &&
+                          bwc + ad[kk] + 4 <= reinterpret_cast<const char *>(Bw + 2 * bplane));
+                dst[kk] = *reinterpret_cast<const float *>(bwc + ad[kk]);
+            }
         };
         // Series of one block (rolling, in block order): u = (C0, C1) parts, m(k-1) = (D0, D1)(k-1)
         // = G_dx1(k-1) + G_dx0(k); pu(k) = u(k) + u(k+1), pm(k) = m(k) + m(k+1); H(j) = pu(j) + pu(j+2)
@@ -859,6 +907,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         };
         auto key_off = [&](int r, int c) {
             const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
+            check_key(a, py, px);
             return (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0);
         };
         // exact merge of (e, n, rank) with the mean key floor(e * 2^13 / n)
@@ -1008,8 +1057,176 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     }
 }
 
+// ---------------------------------------------------------------------------
+// Integer interior body (uint8 SAD, K = 8, interior tiles): DESIGN.md "K1i integer quad body".
+//
+// The same block-grid decomposition as quad_body's interior path, in exact integer arithmetic with
+// two 16-bit lanes per 32-bit register (the (C0, C1) / (D0, D1) series pairs).  Every term is
+// |c - r| <= 255 scaled by 8; every lane sum is <= 8 * 25 * 255 = 51000 < 2^16, so lane arithmetic
+// never carries and sliding-window sums (add the entering, subtract the leaving value: one IADD3)
+// are exact.  Producers: |c - r| (VABSDIFF), the dy lane by IMAD with (8 or 8 << 16), the dx split by
+// a second IMAD and an IADD3, sliding 4-wide H sums (one IADD3 per column and series), one STS per
+// column and series.  Consumers: sliding V sums, the output pair (E(2i), E(2i+1)) =
+// V(i) + (hi V(i), lo V(i+1)) (PRMT + IADD3, which also adds the candidate's position in its group of
+// eight, so each lane holds 8 E + pos), a packed 16-bit min per output pair (ties inside a group go
+// to the lower position = lower rank); every eight candidates the group minima merge into the running
+// best when their E is strictly smaller (earlier groups, i.e. lower ranks, keep ties), with the
+// group index alongside.  Decoded key: E and rank = clist[8 g + pos] (R7 order).
+// ---------------------------------------------------------------------------
+constexpr int kIPitch = kQHC + 1;                        // int plane row pitch (words): rows -> distinct banks
+constexpr int kIPlane = kQHR * kIPitch;                   // words per plane
+constexpr unsigned kIStageBytes = 2u * kIPlane * 4u;      // C plane + D plane
+
+__device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem, int chunk, int px0, int py0) {
+    const int alo = chunk_alo(a.S, chunk);
+    const int ahi = chunk_ahi(a.S, chunk);
+    const int nrow_b = kQWinRows + (ahi - alo);
+    const int ncol_b = kQWinCols + 2 * a.S;
+    const int bpitch = quad_pitch(ncol_b);
+    const int bplane = quad_plane(nrow_b, ncol_b);
+    int *Bw = reinterpret_cast<int *>(smem);
+    unsigned *Hi = reinterpret_cast<unsigned *>(smem + 2 * bplane);   // [kQStages][2 planes][kQHR][kIPitch]
+    int *clist = reinterpret_cast<int *>(Hi + kQStages * 2 * kIPlane);
+    const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {
+        // The window as 32-bit integers, split by row parity like the float body (interior tiles read
+        // only in-frame, in-buffer pixels).
+        const uint8_t *rp = a.ref_p[ref_slot(a)];
+        for (int r = warp; r < nrow_b; r += kNT / 32) {
+            const int y = by0 + r;
+            int *dst = Bw + (r & 1) * bplane + (r >> 1) * bpitch;
+            const uint8_t *src = rp + (int64_t)(y - a.buf_y0) * a.ref.pitch;
+            for (int c = lane; c < ncol_b; c += 32) dst[c] = src[bx0 + c];
+        }
+    }
+    const int k0g = a.chunk_off[chunk], nA = a.chunk_off[chunk + 1] - k0g;
+    for (int i = threadIdx.x; i < nA; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);
+    __syncthreads();
+    if (nA <= 0) return;
+    if (warp < 4) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
+        const int hr = lane, bi = hr - 2;
+        const int pair = warp >> 1, half = warp & 1;
+        int cv[kQGI], ad[kQGI];
+        unsigned W[kQGI], Wd[kQGI];
+#pragma unroll
+        for (int kk = 0; kk < kQGI; ++kk) {
+            const int bk = kQRunI * half - 2 + kk;
+            const int y = py0 + 2 * bi, x = px0 + 2 * bk;
+            // blocks below the frame / the buffer (a band's ragged last tile): weight 0
+            const bool inside = y + 1 < a.H && y + 1 < a.buf_y0 + a.buf_rows;
+            const int64_t r = (int64_t)(y - a.buf_y0);
+            const uint8_t *m0 = a.mask.p + r * a.mask.pitch + x;
+            const int q = !inside ? 0 : m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
+            const int dy = q >> 1, dx = q & 1;
+            cv[kk] = inside ? a.cur.p[(r + dy) * a.cur.pitch + x + dx] : 0;
+            W[kk] = inside ? (dy ? 8u << 16 : 8u) : 0u;            // lane dy, scaled by 8
+            Wd[kk] = dx ? W[kk] : 0u;                               // the dx = 1 part
+            ad[kk] = 4 * (dy * bplane + (bi + 2) * bpitch + (2 * bk + dx + 4 + a.S));
+        }
+        const unsigned hbase = (unsigned)__cvta_generic_to_shared(Hi + hr * kIPitch + kQRunI * half);
+        auto run = [&](auto Pc) {
+            constexpr int P = decltype(Pc)::value;
+            const unsigned hs = hbase + (unsigned)P * kIStageBytes;
+            int rv[kQGI];
+            for (int k = P; k < nA; k += 2) {
+                {
+                    const int pk = clist[k];
+                    const char *bwc = reinterpret_cast<const char *>(
+                        Bw + (((int)(int8_t)(pk & 0xff) - alo) >> 1) * bpitch + (int)(int8_t)((pk >> 8) & 0xff));
+#pragma unroll
+                    for (int kk = 0; kk < kQGI; ++kk) {
+                        QS_DCHECK(bwc + ad[kk] >= reinterpret_cast<const char *>(Bw) &&
+                                  bwc + ad[kk] + 4 <= reinterpret_cast<const char *>(Bw + 2 * bplane));
+                        rv[kk] = *reinterpret_cast<const int *>(bwc + ad[kk]);
+                    }
+                }
+                if (k >= 2) nb_sync_i<5 + P, kQBarI>();                 // EMPTY[P]
+                unsigned u[kQGI], g[kQGI], m[kQGI - 1], hc = 0, hd = 0;
+#pragma unroll
+                for (int kk = 0; kk < kQGI; ++kk) {
+                    const unsigned t = __usad((unsigned)cv[kk], (unsigned)rv[kk], 0u);   // |c - r|
+                    u[kk] = t * W[kk];
+                    g[kk] = t * Wd[kk];
+                    if (kk > 0) m[kk - 1] = g[kk - 1] + (u[kk] - g[kk]);   // D(k-1) = G_dx1(k-1) + G_dx0(k)
+                    if (kk == 3) hc = u[0] + u[1] + u[2] + u[3];
+                    else if (kk > 3 && kk - 3 < kQRunI) hc = hc + u[kk] - u[kk - 4];
+                    if (kk >= 3 && kk - 3 < kQRunI)
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(hs + 4u * (kk - 3)), "r"(hc) : "memory");
+                    if (kk == 4) hd = m[0] + m[1] + m[2] + m[3];
+                    else if (kk > 4 && kk - 4 < kQRunI) hd = hd + m[kk - 1] - m[kk - 5];
+                    if (kk >= 4 && kk - 4 < kQRunI)
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(hs + 4u * (kIPlane + kk - 4)), "r"(hd) : "memory");
+                }
+                nb_arrive_i<1 + P, kQBarI>();                           // FULL[P]
+            }
+            if (P < nA) nb_sync_i<5 + P, kQBarI>();                    // drain
+        };
+        if (pair == 0) run(std::integral_constant<int, 0>{});
+        else run(std::integral_constant<int, 1>{});
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
+        const int j = lane;
+        const int cw = warp - 4, pl = cw & 1, i0 = kQSeg * (cw >> 1);
+        unsigned gmin[kQSeg], best[kQSeg], bestg[kQSeg];
+#pragma unroll
+        for (int r = 0; r < kQSeg; ++r) { gmin[r] = 0xffffffffu; best[r] = 0xffffffffu; bestg[r] = 0u; }
+        const unsigned cbase = (unsigned)__cvta_generic_to_shared(Hi + pl * kIPlane + i0 * kIPitch + j);
+        auto consume = [&](int k, auto Pc) {
+            constexpr int P = decltype(Pc)::value;
+            nb_sync_i<1 + P, kQBarI>();                                 // FULL[P]
+            const unsigned cs = cbase + (unsigned)P * kIStageBytes;
+            unsigned x[kQSeg + 4];
+#pragma unroll
+            for (int t = 0; t < kQSeg + 4; ++t)
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x[t]) : "r"(cs + 4u * t * kIPitch) : "memory");
+            nb_arrive_i<5 + P, kQBarI>();                               // EMPTY[P]
+            const unsigned pos2 = (unsigned)(k & 7) * 0x10001u;
+            unsigned v = x[0] + x[1] + x[2] + x[3];
+#pragma unroll
+            for (int r = 0; r < kQSeg; ++r) {
+                const unsigned vn = v + x[r + 4] - x[r];                // V(r + 1)
+                const unsigned e = v + __byte_perm(v, vn, 0x5432) + pos2;   // (8 E(2i) + pos, 8 E(2i+1) + pos)
+                gmin[r] = __vminu2(gmin[r], e);
+                v = vn;
+            }
+            if ((k & 7) == 7 || k == nA - 1) {
+                // group end: a lane takes the group's minimum iff its E is strictly smaller (the
+                // positions inside a group are not comparable across groups): 8 E_g + 7 < 8 E_best.
+                const unsigned g2 = (unsigned)(k >> 3) * 0x10001u;
+#pragma unroll
+                for (int r = 0; r < kQSeg; ++r) {
+                    const unsigned lt = __vcmpltu2(gmin[r] | 0x00070007u, best[r] & 0xfff8fff8u);
+                    best[r] = (best[r] & ~lt) | (gmin[r] & lt);
+                    bestg[r] = (bestg[r] & ~lt) | (g2 & lt);
+                    gmin[r] = 0xffffffffu;
+                }
+            }
+        };
+        for (int k = 0; k < nA; k += 2) {
+            consume(k, std::integral_constant<int, 0>{});
+            if (k + 1 < nA) consume(k + 1, std::integral_constant<int, 1>{});
+        }
+#pragma unroll
+        for (int r = 0; r < kQSeg; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
+                const unsigned val = c ? best[r] >> 16 : best[r] & 0xffffu;
+                if (val == 0xffffu || py >= a.oy1 || px >= a.ox1) continue;
+                const unsigned gi = c ? bestg[r] >> 16 : bestg[r] & 0xffffu;
+                const int rank = clist[8 * gi + (val & 7u)] >> 16;
+                const unsigned long long key =
+                    ((unsigned long long)__float_as_uint((float)(val >> 3)) << 32) | (unsigned)rank;
+                check_key(a, py, px);
+        atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+            }
+    }
+}
+
 template <int K, bool EXACT, bool SSD, bool REV>
-__global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
+__global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ BoxArgs a) {
     extern __shared__ __align__(16) float smem[];
     const int unit = blockIdx.x / a.n_ref;   // the slots of one unit run side by side
     const int chunk = unit % a.n_chunks;
@@ -1038,6 +1255,12 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const BoxArgs a) {
                                   (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1) &&
                                   (py0 - 4 - a.S >= a.buf_y0) && (ylast + 3 + a.S < a.buf_y0 + a.buf_rows);
                 if (geom) {
+                    if constexpr (EXACT && !SSD) {
+                        if (a.int_body) {   // uint8 SAD: the integer body
+                            quad_interior_int(a, smem, chunk, px0, py0);
+                            return;
+                        }
+                    }
                     quad_body<SSD, EXACT, false>(a, smem, chunk, px0, py0);
                     return;
                 }
@@ -1063,7 +1286,8 @@ cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
                   sizeof(int) * kChunkRows * (2 * a.S + 1);
     if (K == 8 && !REV) {
         const int qrows = kQWinRows + kChunkSpan - 1, qcols = kQWinCols + 2 * a.S;
-        const size_t qs = sizeof(float) * 2 * (size_t)quad_plane(qrows, qcols) +
+        const size_t plane = a.tma ? (size_t)((a.tma_rows * a.tma_cols + 31) & ~31) : (size_t)quad_plane(qrows, qcols);
+        const size_t qs = sizeof(float) * 2 * plane +
                           sizeof(f2_t) * kQStages * kQPlanes * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8);
         smem = smem > qs ? smem : qs;
     }

@@ -5,12 +5,15 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
+
+#include <cudaTypedefs.h>
 
 #include "qs_internal.cuh"
 
@@ -265,9 +268,61 @@ size_t ws_slot_bytes(const Roi &r, int S) {
     return std::max(ws_layout(me, 1, true, true).total, ws_layout(rme, 1, true, false).total);
 }
 
+// uint8 SAD interior tiles: the integer packed body (default) or the fp32 body (QS_U8_BODY=float;
+// kept for the measured comparison in DESIGN.md).
+int u8_int_body() {
+    const char *e = getenv("QS_U8_BODY");   // read per call (cheap), so a process can switch
+    return (e && !strcmp(e, "float")) ? 0 : 1;
+}
+
+// TMA staging of the float reference window (me_box quad body): QS_TMA=1
+// enables it (measured against the cp.async staging; see DESIGN.md for the default).
+int tma_enabled() {
+    const char *e = getenv("QS_TMA");   // read per call (cheap), so a process can switch
+    return (e && !strcmp(e, "1")) ? 1 : 0;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }();
+    return fn;
+}
+
+// Descriptors for slots 0..n-1 of a float-reference K = 8 forward launch: the buffer viewed as
+// [buf_rows / 2][2][W] floats (row pairs, parity, column), box [tma_rows][1][tma_cols], NaN fill.
+// Leaves a.tma = 0 (cp.async staging) when disabled or not applicable (odd buffer rows).
+void set_tma(BoxArgs &a, int n) {
+    a.tma = 0;
+    if (!tma_enabled() || !a.ref_f32 || (a.buf_rows & 1) || a.buf_rows < 2) return;
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return;
+    const int cols = (kQWinColsHost + 2 * a.S + 3) & ~3;
+    const int rows = (kQWinRowsHost + kChunkSpan - 1 + 1) / 2;
+    for (int i = 0; i < n; ++i) {
+        const cuuint64_t dims[3] = {(cuuint64_t)a.W, 2, (cuuint64_t)(a.buf_rows / 2)};
+        const cuuint64_t strides[2] = {(cuuint64_t)a.ref.pitch, (cuuint64_t)(2 * a.ref.pitch)};
+        const cuuint32_t box[3] = {(cuuint32_t)cols, 1, (cuuint32_t)rows};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (enc(&a.tmap[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<uint8_t *>(a.ref_p[i]), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA) != CUDA_SUCCESS)
+            return;
+    }
+    a.tma_cols = cols;
+    a.tma_rows = rows;
+    a.tma = 1;
+}
+
 BoxArgs box_args(const Roi &r, const uint8_t *cur, const uint8_t *mask, int64_t cur_pitch, const void *ref,
                  int64_t ref_pitch, const qs_me_params *p, const CandTables *t) {
     BoxArgs a{};
+    a.int_body = u8_int_body();
     a.cur = Plane{cur, cur_pitch};
     a.mask = Plane{mask, cur_pitch};
     a.ref = Plane{static_cast<const uint8_t *>(ref), ref_pitch};
@@ -433,6 +488,8 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     a.keys = keys;
     a.key_pitch = r.W;
     a.s2 = s2;
+    a.ref_p[0] = a.ref.p;
+    if (K == 8) set_tma(a, 1);
     {
         ProfScope ps(P_ME_BOX, s);
         e = launch_box(a, K, p->err == QS_SSD, false, s);
@@ -641,6 +698,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
             a.s2_p[i] = f32 ? reinterpret_cast<unsigned *>(wg + L.s2 + s2a * i) : nullptr;
         }
         a.s2 = a.s2_p[0];
+        set_tma(a, n);
         {
             ProfScope ps(P_ME_BOX, s);
             e = launch_box(a, 8, p->err == QS_SSD, false, s);

@@ -4,7 +4,27 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+#include <cuda.h>           // CUtensorMap (TMA descriptors; the driver entry point is resolved at run time)
 #include <cuda_runtime.h>
+
+// Bounds checks of the checked build (libqs_checked.so, -DQS_CHECKED): the
+// staged-window reads, the shared ring and the global key / field writes trap when out of range.
+// The product build compiles them out.
+#ifdef QS_CHECKED
+#define QS_DCHECK(cond)                                                                     \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            printf("QS_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                      \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define QS_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 
 #include "../../include/qs.h"
 
@@ -31,6 +51,8 @@ constexpr int kChunkRows = 7;  // alpha rows of candidates per work unit
 // dy for every candidate -- the quad body's reference window is split by row parity (conflict-light
 // gathers, me_box.cu).  kChunkSpan = rows spanned by a chunk's window.
 constexpr int kChunkSpan = 2 * kChunkRows - 1;
+constexpr int kQWinRowsHost = 64;   // quad body window: pixel rows of the tile's blocks (me_box.cuh kQWinRows)
+constexpr int kQWinColsHost = 72;   // and pixel columns (me_box.cuh kQWinCols)
 __host__ __device__ constexpr int chunk_alo(int S, int chunk) { return -S + 2 * kChunkRows * (chunk >> 1) + (chunk & 1); }
 __host__ __device__ constexpr int chunk_ahi(int S, int chunk) {
     return chunk_alo(S, chunk) + kChunkSpan - 1 < S ? chunk_alo(S, chunk) + kChunkSpan - 1 : S;
@@ -81,6 +103,13 @@ struct BoxArgs {
     // float bits ([oy1-oy0][key_pitch], 0xffffffff = none).  nullptr for uint8 references.
     unsigned *s2;
     unsigned *s2_p[kMaxRefs];
+    int int_body;                    // uint8 SAD interior tiles: 1 = integer packed body, 0 = fp32 body
+    // TMA staging of the quad body's float reference window: one 3-D tiled
+    // descriptor per slot over the buffer as [rows / 2][parity][W] floats, boxes of
+    // [tma_rows][1][tma_cols] (one per row-parity plane), out-of-frame / out-of-buffer elements
+    // filled with NaN ("no term").  tma = 0: cp.async / register staging.
+    int tma, tma_cols, tma_rows;
+    CUtensorMap tmap[kMaxRefs];
 };
 
 // Certified float argmin.  The float consumers track, per output,

@@ -203,6 +203,8 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
         // the accumulation order is the definition's row-major order.
 #pragma unroll 1
         for (int oy = 0; oy < kFK && settled != 0x7fu; ++oy) {
+            QS_DCHECK(crow + oy >= 0 && crow + oy < g.CR && ccol >= 0 && ccol + kSeg <= g.cpitch);
+            QS_DCHECK(rrow + oy >= 0 && rrow + oy < g.RR && rcol >= 0 && rcol + kFK <= g.rpitch);
             const float *cp = g.Cs + (crow + oy) * g.cpitch + ccol;
             const float *rp = g.Rs + (rrow + oy) * g.rpitch + rcol;
             float c[kSeg], r[kFK];
@@ -244,6 +246,8 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
     } else {
 #pragma unroll 1
     for (int oy = 0; oy < kFK && settled != 0x7fu; ++oy) {
+        QS_DCHECK(crow + oy >= 0 && crow + oy < g.CR && ccol >= 0 && ccol + kSeg <= g.cpitch);
+        QS_DCHECK(rrow + oy >= 0 && rrow + oy < g.RR && rcol >= 0 && rcol + kFK <= g.rpitch);
         const float *cp = g.Cs + (crow + oy) * g.cpitch + ccol;
         const float *rp = g.Rs + (rrow + oy) * g.rpitch + rcol;
         float c[kSeg], r[kFK];

@@ -844,3 +844,17 @@ def test_projection_only_mode(cfg):
     with pytest.raises(qs.QsError):   # projection-only needs the fused K = 8 path
         qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H), qs.make_params(K=7, S=S, ref_f32=c.ref_f32), None,
                              fuse=qs.make_checks(), project=(pvs, pms, s, cn))
+
+
+@pytest.mark.parametrize("env,val,f32", [("QS_TMA", "1", True), ("QS_U8_BODY", "float", False)])
+def test_staging_and_body_variants_bit_exact(env, val, f32, monkeypatch):
+    """The measured alternatives stay exact: TMA staging of the float window (QS_TMA=1) and the fp32
+    body for uint8 interior tiles (QS_U8_BODY=float) give the oracle's planes, interior and border."""
+    monkeypatch.setenv(env, val)
+    seq = synth.make_sequence(4 if f32 else 2, w=320, h=256)
+    for t, d in ((5, 1), (6, 3)):
+        inp = synth.pair_inputs(seq, t, d)
+        g, gev = gpu_me(inp, K=8, S=16, fuse=qs.make_checks())
+        o, oev = oracle.pair_chain(inp, K=8, S=16, check="nnc_frmc", threads=_THREADS)
+        assert_field_equal(g, o, what=f"{env}={val} t={t} d={d}")
+        assert gev == oev

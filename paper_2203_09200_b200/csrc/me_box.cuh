@@ -536,6 +536,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             for (int p = 0; p < 2; ++p) {
                 const int b = by0 + p - a.buf_y0;   // buffer row of window row p
                 const unsigned dst = (unsigned)__cvta_generic_to_shared(Bw + p * bplane);
+                QS_DCHECK((dst & 127u) == 0u);
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                     ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tm)), "r"(bx0), "r"(b & 1), "r"(b >> 1), "r"(bar)
@@ -1227,7 +1228,7 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
 
 template <int K, bool EXACT, bool SSD, bool REV>
 __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ BoxArgs a) {
-    extern __shared__ __align__(16) float smem[];
+    extern __shared__ __align__(1024) float smem[];   // TMA box destinations need 128-byte alignment
     const int unit = blockIdx.x / a.n_ref;   // the slots of one unit run side by side
     const int chunk = unit % a.n_chunks;
     const int tile = unit / a.n_chunks;

@@ -299,7 +299,9 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // Leaves a.tma = 0 (cp.async staging) when disabled or not applicable (odd buffer rows).
 void set_tma(BoxArgs &a, int n) {
     a.tma = 0;
-    if (!tma_enabled() || !a.ref_f32 || (a.buf_rows & 1) || a.buf_rows < 2) return;
+    // The box's first column px0 - 4 - S must sit on a 16-byte boundary (tiles start at multiples of
+    // 64 columns): S % 4 == 0 (config 4's S = 24; other S keep the cp.async staging).
+    if (!tma_enabled() || !a.ref_f32 || (a.buf_rows & 1) || a.buf_rows < 2 || (a.S & 3)) return;
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return;
     const int cols = (kQWinColsHost + 2 * a.S + 3) & ~3;

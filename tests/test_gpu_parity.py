@@ -858,3 +858,54 @@ def test_staging_and_body_variants_bit_exact(env, val, f32, monkeypatch):
         o, oev = oracle.pair_chain(inp, K=8, S=16, check="nnc_frmc", threads=_THREADS)
         assert_field_equal(g, o, what=f"{env}={val} t={t} d={d}")
         assert gev == oev
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_u8_row_bands_equal_full_frame_config5(G):
+    """P14 on the 4K config (S = 32, halo 38 rows): sequence 0 of config 5 at full size cut by
+    rowband.plan_bands; each band runs qs_me_search_refs (d = 1..3, fused cascade and PR) with buffers
+    holding only band + halo rows.  The union equals the full-frame call bit for bit; the rows at each
+    cut equal the oracle's chain."""
+    from paper_2203_09200_b200 import rowband
+    c = synth.CONFIGS[5]
+    seq = synth.make_sequence(5)
+    t, S, K = 5, c.S, 8
+    inps = [synth.pair_inputs(seq, t, d) for d in (1, 2, 3)]
+    H, W = c.h, c.w
+    prm = qs.make_params(K=K, S=S)
+
+    def run(y0, y1, b0, b1):
+        br = b1 - b0
+        cur = qs.to_plane(inps[0]["cur"][b0:b1], DEV_)
+        msk = qs.to_plane(inps[0]["cur_mask"][b0:b1], DEV_)
+        refs = [qs.to_plane(i["ref"][b0:b1], DEV_) for i in inps]
+        pvs = [qs.to_plane(i["past_val"][b0:b1], DEV_) for i in inps]
+        pms = [qs.to_plane(i["past_mask"][b0:b1], DEV_) for i in inps]
+        outs = [qs.Field.alloc(br, W, False, DEV_) for _ in inps]
+        s, cn = qs.alloc_acc(br, W, DEV_)
+        qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H, y0, y1, b0, br), prm, outs,
+                             fuse=qs.make_checks(), project=(pvs, pms, s, cn))
+        torch.cuda.synchronize()
+        fs = []
+        for o in outs:
+            g = o.numpy()
+            g["err"] = g["err"].view(np.uint32)
+            fs.append({k: v[y0 - b0:y1 - b0] for k, v in g.items()})
+        return fs, s.cpu().numpy().view(np.uint32)[y0 - b0:y1 - b0], cn.cpu().numpy()[y0 - b0:y1 - b0]
+
+    full, fsum, fcnt = run(0, H, 0, H)
+    cuts = rowband.plan_bands(G, H, S, K)
+    halo = rowband.halo_rows(S, K)
+    assert halo == 38
+    for r in range(G):
+        y0, y1 = cuts[r], cuts[r + 1]
+        fs, bsum, bcnt = run(y0, y1, max(0, y0 - halo), min(H, y1 + halo))
+        for d, (bf, ff) in enumerate(zip(fs, full), 1):
+            for k in ("alpha", "beta", "count", "status", "err"):
+                assert np.array_equal(bf[k], ff[k][y0:y1]), (G, r, d, k)
+        assert np.array_equal(bsum, fsum[y0:y1]) and np.array_equal(bcnt, fcnt[y0:y1]), (G, r)
+    for y in cuts[1:-1]:
+        rows = (y - 1, y + 1)
+        for ff, inp in zip(full, inps):
+            o, _ = oracle.pair_chain(inp, K=K, S=S, check="nnc_frmc", rows=rows, threads=_THREADS)
+            assert_field_equal(ff, o, rows=rows, what=f"config 5 cut {y}")

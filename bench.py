@@ -347,7 +347,9 @@ def run_ours(args):
         out = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
                "higher_is_better": True, "scaling": "weak" if args.sequences else "strong", "vs_baseline": None,
-               "dtype": "f32" if f32 else "u8->f32(exact)", "data": "synthetic",
+               "dtype": "f32" if f32 else ("u8 (int16x2 interior body, exact fp32 border tiles)"
+                                            if os.environ.get("QS_U8_BODY") != "float" else "u8->f32(exact)"),
+               "data": "synthetic",
                "config": {"workload": cfg.name, "frame": f"{W}x{H}", "K": K, "S": S, "refs": 3,
                           "mask": "dynamic" if cfg.dynamic else "fixed", "check": args.check,
                           "parallelism": (f"sequences{world}" if args.sequences else f"rowband{world}") if world > 1

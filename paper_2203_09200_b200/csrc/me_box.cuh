@@ -1255,6 +1255,9 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ Box
                 const bool geom = (py0 - 4 - a.S >= 0) && (ylast + 3 + a.S <= a.H - 1) &&
                                   (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1) &&
                                   (py0 - 4 - a.S >= a.buf_y0) && (ylast + 3 + a.S < a.buf_y0 + a.buf_rows);
+#ifdef QS_EXP_SKIP   // measurement builds only (tools/build_exp.sh): 1 = skip border tiles, 2 = skip interior
+                if ((QS_EXP_SKIP == 1 && !geom) || (QS_EXP_SKIP == 2 && geom)) return;
+#endif
                 if (geom) {
                     if constexpr (EXACT && !SSD) {
                         if (a.int_body) {   // uint8 SAD: the integer body

@@ -909,3 +909,39 @@ def test_u8_row_bands_equal_full_frame_config5(G):
         for ff, inp in zip(full, inps):
             o, _ = oracle.pair_chain(inp, K=K, S=S, check="nnc_frmc", rows=rows, threads=_THREADS)
             assert_field_equal(ff, o, rows=rows, what=f"config 5 cut {y}")
+
+
+@pytest.mark.parametrize("cfg,ds", [(3, (1, 2, 3))])
+def test_fullsize_u8_full_frame_bit_exact(cfg, ds):
+    """A whole frame of config 3 in the bench's launch (qs_me_search_refs, fused cascade and PR; the
+    integer interior body and the exact fp32 border body) against the oracle's chain over every row and
+    all three references.  (A config-5 frame is ~8 min of 16-core oracle time per reference; config 5
+    is checked on sampled rows, frame edges and the row-band cuts.)"""
+    c = synth.CONFIGS[cfg]
+    seq = synth.make_sequence(cfg)
+    t = 5
+    inps = [synth.pair_inputs(seq, t, d) for d in ds]
+    H, W = c.h, c.w
+    cur = qs.to_plane(inps[0]["cur"], DEV_)
+    msk = qs.to_plane(inps[0]["cur_mask"], DEV_)
+    refs = [qs.to_plane(i["ref"], DEV_) for i in inps]
+    pvs = [qs.to_plane(i["past_val"], DEV_) for i in inps]
+    pms = [qs.to_plane(i["past_mask"], DEV_) for i in inps]
+    outs = [qs.Field.alloc(H, W, False, DEV_) for _ in inps]
+    s, cn = qs.alloc_acc(H, W, DEV_)
+    ev = torch.zeros(1, dtype=torch.int64, device=DEV_)
+    qs.qs_me_search_refs(cur, msk, refs, qs.make_roi(W, H), qs.make_params(K=8, S=c.S), outs,
+                         fuse=qs.make_checks(), project=(pvs, pms, s, cn), eval_count=ev)
+    torch.cuda.synchronize()
+    osum = np.zeros((H, W), np.uint32)
+    ocnt = np.zeros((H, W), np.uint8)
+    oev = 0
+    for d, (o_f, inp) in zip(ds, zip(outs, inps)):
+        g = o_f.numpy()
+        g["err"] = g["err"].view(np.uint32)
+        o, e = oracle.pair_chain(inp, K=8, S=c.S, check="nnc_frmc", threads=_THREADS)
+        assert_field_equal(g, o, what=f"config {cfg} full frame d={d}")
+        osum, ocnt = oracle.project(o, inp["past_val"], inp["past_mask"], osum, ocnt)
+        oev += e
+    assert np.array_equal(s.cpu().numpy().view(np.uint32), osum) and np.array_equal(cn.cpu().numpy(), ocnt)
+    assert int(ev.item()) == oev

@@ -314,14 +314,14 @@ __device__ __forceinline__ void box_body(const BoxArgs &a, float *smem, int chun
         const int py = py0 + sb * kSeg + i, px = px0 + xb;
         if constexpr (!EXACT) {
             // float: keyed winner (e for n constant, else e * rcp(n)) and second, certified later
-            if (!(be[i] < kAdmissibleMax) || py >= a.oy1 || px >= a.ox1) continue;
+            if (!(be[i] < kAdmissibleMax) || py < a.oy0 || py >= a.oy1 || px >= a.ox1) continue;
             check_key(a, py, px);
             const int64_t o = (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0);
             const int rank = clist[__float_as_uint(be[i]) & kKeyBits] >> 16;
             merge_f32(a.keys_p[ref_slot(a)] + o, a.s2_p[ref_slot(a)] + o, fkey_val(be[i]), rank, fkey_val2(bn[i]));
             continue;
         }
-        if (br[i] < 0 || py >= a.oy1 || px >= a.ox1) continue;
+        if (br[i] < 0 || py < a.oy0 || py >= a.oy1 || px >= a.ox1) continue;
         unsigned long long hi;
         if constexpr (!CNT) {
             hi = __float_as_uint(be[i]);                 // e (interior: n constant): non-negative float
@@ -746,7 +746,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 for (int c = 0; c < 2; ++c) {
                     const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
                     if constexpr (FK) {
-                        if (!(be[r][c] < kAdmissibleMax) || py >= a.oy1 || px >= a.ox1) continue;
+                        if (!(be[r][c] < kAdmissibleMax) || py < a.oy0 || py >= a.oy1 || px >= a.ox1) continue;
                         check_key(a, py, px);
                         const int64_t o = (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0);
                         merge_f32(a.keys_p[ref_slot(a)] + o, a.s2_p[ref_slot(a)] + o, fkey_val(be[r][c]),
@@ -758,7 +758,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                             br[r][c] = clist[kv & 511u] >> 16;
                             be[r][c] = (float)(kv >> 9);
                         }
-                        if (br[r][c] < 0 || py >= a.oy1 || px >= a.ox1) continue;
+                        if (br[r][c] < 0 || py < a.oy0 || py >= a.oy1 || px >= a.ox1) continue;
                         const unsigned long long key =
                             ((unsigned long long)__float_as_uint(be[r][c]) << 32) | (unsigned)br[r][c];
                         check_key(a, py, px);
@@ -1215,7 +1215,7 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
             for (int c = 0; c < 2; ++c) {
                 const int py = py0 + 2 * (i0 + r) + c, px = px0 + 2 * j + pl;
                 const unsigned val = c ? best[r] >> 16 : best[r] & 0xffffu;
-                if (val == 0xffffu || py >= a.oy1 || px >= a.ox1) continue;
+                if (val == 0xffffu || py < a.oy0 || py >= a.oy1 || px >= a.ox1) continue;
                 const unsigned gi = c ? bestg[r] >> 16 : bestg[r] & 0xffffu;
                 const int rank = clist[8 * gi + (val & 7u)] >> 16;
                 const unsigned long long key =
@@ -1237,7 +1237,9 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ Box
     // rows are scheduled in the first waves, not in the tail.
     const int q = tile / a.tiles_x, T = a.tiles_y;
     const int tyi = T < 3 ? q : (q == 0 ? 0 : q == 1 ? T - 1 : q == 2 ? T - 2 : q - 2);
-    const int px0 = a.ox0 + txi * kTX, py0 = a.oy0 + tyi * kTY;
+    // tile_off (forward K = 8 launches): the tile grid starts tile_off rows above oy0, placed by the
+    // host so that the fewest tile rows reach outside the frame (border tiles cost ~1.7x).
+    const int px0 = a.ox0 + txi * kTX, py0 = a.oy0 - a.tile_off + tyi * kTY;
     constexpr int KL = K / 2, KR = K - 1 - K / 2;
     bool interior = !REV && (py0 - KL - a.S >= 0) && (py0 + kTY - 1 + KR + a.S <= a.H - 1) &&
                     (px0 - KL - a.S >= 0) && (px0 + kTX - 1 + KR + a.S <= a.W - 1);

@@ -321,6 +321,32 @@ void set_tma(BoxArgs &a, int n) {
     a.tma = 1;
 }
 
+// Tile rows of a forward K = 8 launch over output rows [lo, hi): the grid offset (rows of the first
+// tile above lo; lo - offset even) with the fewest tile rows whose windows and candidates reach outside the frame or the
+// buffer (those run the slower border body), then the fewest tile rows.  Results do not depend on it.
+void place_tile_rows(BoxArgs &a, const Roi &r, int lo, int hi) {
+    const int S = a.S, top = std::max(0, r.b0), bot = std::min(r.H, r.b0 + r.br) - 1;
+    int best_off = 0, best_border = 1 << 30, best_rows = 1 << 30;
+    // lo - off even: the quad body's 2x2 blocks stay on the mask's block grid (odd tile rows would send
+    // every tile to the generic body)
+    for (int off = lo & 1; off < kTY; off += 2) {
+        const int rows = (hi - lo + off + kTY - 1) / kTY;
+        int border = 0;
+        for (int t = 0; t < rows; ++t) {
+            const int py0 = lo - off + t * kTY;
+            const int ylast = std::min(py0 + kTY, hi) - 1;   // the outputs the merge keeps
+            if (py0 - 4 - S < top || ylast + 3 + S > bot || std::max(py0, lo) - 4 - S < top) ++border;
+        }
+        if (border < best_border || (border == best_border && rows < best_rows)) {
+            best_off = off;
+            best_border = border;
+            best_rows = rows;
+        }
+    }
+    a.tile_off = best_off;
+    a.tiles_y = best_rows;
+}
+
 BoxArgs box_args(const Roi &r, const uint8_t *cur, const uint8_t *mask, int64_t cur_pitch, const void *ref,
                  int64_t ref_pitch, const qs_me_params *p, const CandTables *t) {
     BoxArgs a{};
@@ -487,6 +513,7 @@ int qs_me_search(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_pitch,
     a.ox1 = r.W;
     a.tiles_x = (r.W + kTX - 1) / kTX;
     a.tiles_y = (hi - lo + kTY - 1) / kTY;
+    if (K == 8) place_tile_rows(a, r, lo, hi);
     a.keys = keys;
     a.key_pitch = r.W;
     a.s2 = s2;
@@ -691,6 +718,7 @@ int qs_me_search_refs(const uint8_t *cur, const uint8_t *cur_mask, int64_t cur_p
         a.ox1 = r.W;
         a.tiles_x = (r.W + kTX - 1) / kTX;
         a.tiles_y = (hi - lo + kTY - 1) / kTY;
+        place_tile_rows(a, r, lo, hi);
         a.keys = reinterpret_cast<unsigned long long *>(wg);
         a.key_pitch = r.W;
         a.n_ref = n;

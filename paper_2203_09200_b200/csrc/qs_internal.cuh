@@ -91,6 +91,7 @@ struct BoxArgs {
     int S, min_support;
     int oy0, oy1, ox0, ox1;          // output domain (rows / cols, frame coords; may exceed the frame for REV)
     int tiles_x, tiles_y, n_chunks;
+    int tile_off;                    // rows of the first tile above oy0 (0 .. kTY-1)
     const int32_t *chunked;
     const int32_t *chunk_off;
     unsigned long long *keys;        // [oy1-oy0][key_pitch] (slot 0)

@@ -497,7 +497,8 @@ __host__ __device__ constexpr int quad_pitch(int cols) { return 2 * (((cols + 1)
 __host__ __device__ constexpr int quad_plane(int rows, int cols) { return (((rows + 1) / 2) * quad_pitch(cols) + 31) & ~31; }
 
 template <bool SSD, bool EXACT, bool BORDER>
-__device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0) {
+__device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0,
+                                          bool skip_phase1 = false) {
     constexpr bool Q2 = BORDER && !(EXACT && SSD);
     const int alo = chunk_alo(a.S, chunk);
     const int ahi = chunk_ahi(a.S, chunk);
@@ -599,9 +600,11 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         }
     }
     __syncthreads();
+    int a0 = nA;   // list position of list B
     if constexpr (BORDER) {
-        nA = nsel[0];
-        nB = Q2 ? nsel[1] - nA : 0;
+        a0 = nsel[0];
+        nB = Q2 ? nsel[1] - a0 : 0;
+        nA = skip_phase1 ? 0 : a0;   // phase 1 already done (uint8: the integer body)
     }
     const int e1 = nA + ((BORDER && nA > 0) ? 1 : 0);   // entries of phase 1 (+ the npx entry)
     const int n_ent = e1 + nB;
@@ -876,7 +879,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             if (nA & 1) produce(nA, 1, ra, rb, -1, 1);
             else produce(nA, 0, ra, rb, -1, 1);
         }
-        if constexpr (Q2) run(nA, nB, e1, 2);
+        if constexpr (Q2) run(a0, nB, e1, 2);
         for (int k = max(0, n_ent - kQStages); k < n_ent; ++k) nb_sync(5 + (k & (kQStages - 1)), kNT);   // drain
     } else {
         // ------------------------------ consumer ------------------------------
@@ -1037,13 +1040,13 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 };
                 if ((e1 & 1) == 0) {
                     for (int i = 0; i < nB; i += 2) {
-                        consume2(nA + i, 0);
-                        if (i + 1 < nB) consume2(nA + i + 1, 1);
+                        consume2(a0 + i, 0);
+                        if (i + 1 < nB) consume2(a0 + i + 1, 1);
                     }
                 } else {
                     for (int i = 0; i < nB; i += 2) {
-                        consume2(nA + i, 1);
-                        if (i + 1 < nB) consume2(nA + i + 1, 0);
+                        consume2(a0 + i, 1);
+                        if (i + 1 < nB) consume2(a0 + i + 1, 0);
                     }
                 }
 #pragma unroll
@@ -1078,6 +1081,13 @@ constexpr int kIPitch = kQHC + 1;                        // int plane row pitch 
 constexpr int kIPlane = kQHR * kIPitch;                   // words per plane
 constexpr unsigned kIStageBytes = 2u * kIPlane * 4u;      // C plane + D plane
 
+// BRD (border tiles, round 2): the same body runs phase 1 of a uint8 SAD border tile -- its clip-free
+// candidates (tile_clip_free: n(p, v) = npx(p) for all of them) -- with bounds-checked staging (0
+// outside the frame / buffer), weight 0 for blocks outside, one extra ring entry with t = 1 per
+// measured in-frame block (its sums are 8 npx), and the border body's mean key floor(e 2^13 / npx);
+// the caller then runs the border body's phase 2 on the other candidates.  Returns after the
+// setmaxnreg roles are restored (128 registers everywhere), so a body may follow.
+template <bool BRD>
 __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem, int chunk, int px0, int py0) {
     const int alo = chunk_alo(a.S, chunk);
     const int ahi = chunk_ahi(a.S, chunk);
@@ -1088,23 +1098,52 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
     int *Bw = reinterpret_cast<int *>(smem);
     unsigned *Hi = reinterpret_cast<unsigned *>(smem + 2 * bplane);   // [kQStages][2 planes][kQHR][kIPitch]
     int *clist = reinterpret_cast<int *>(Hi + kQStages * 2 * kIPlane);
+    int *ncnt = clist + kChunkRows * (2 * a.S + 1);
     const int by0 = py0 - 4 + alo, bx0 = px0 - 4 - a.S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     {
         // The window as 32-bit integers, split by row parity like the float body (interior tiles read
-        // only in-frame, in-buffer pixels).
+        // only in-frame, in-buffer pixels; border tiles store 0 outside).
         const uint8_t *rp = a.ref_p[ref_slot(a)];
         for (int r = warp; r < nrow_b; r += kNT / 32) {
             const int y = by0 + r;
             int *dst = Bw + (r & 1) * bplane + (r >> 1) * bpitch;
             const uint8_t *src = rp + (int64_t)(y - a.buf_y0) * a.ref.pitch;
-            for (int c = lane; c < ncol_b; c += 32) dst[c] = src[bx0 + c];
+            if (BRD) {
+                const bool row_in = y >= 0 && y < a.H && y >= a.buf_y0 && y < a.buf_y0 + a.buf_rows;
+                for (int c = lane; c < ncol_b; c += 32) {
+                    const int x = bx0 + c;
+                    dst[c] = (row_in && x >= 0 && x < a.W) ? src[x] : 0;
+                }
+            } else {
+                for (int c = lane; c < ncol_b; c += 32) dst[c] = src[bx0 + c];
+            }
         }
     }
-    const int k0g = a.chunk_off[chunk], nA = a.chunk_off[chunk + 1] - k0g;
-    for (int i = threadIdx.x; i < nA; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);
+    const int k0g = a.chunk_off[chunk], nkc = a.chunk_off[chunk + 1] - k0g;
+    if (!BRD) {
+        for (int i = threadIdx.x; i < nkc; i += kNT) clist[i] = __ldg(a.chunked + k0g + i);
+    } else if (warp == 0) {
+        // the tile's clip-free candidates, in rank order
+        int n = 0;
+        for (int base = 0; base < nkc; base += 32) {
+            const int i = base + lane;
+            int pk = 0;
+            bool keep = false;
+            if (i < nkc) {
+                pk = __ldg(a.chunked + k0g + i);
+                keep = tile_clip_free<8>(a, px0, py0, (int)(int8_t)(pk & 0xff), (int)(int8_t)((pk >> 8) & 0xff));
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) clist[n + __popc(m & ((1u << lane) - 1u))] = pk;
+            n += __popc(m);
+        }
+        if (lane == 0) ncnt[0] = n;
+    }
     __syncthreads();
-    if (nA <= 0) return;
+    const int nA = BRD ? ncnt[0] : nkc;
+    if (nA <= 0) return;                                              // uniform
+    const int NE = nA + (BRD ? 1 : 0);                                // entries (+ the npx entry)
     if (warp < 4) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
         const int hr = lane, bi = hr - 2;
@@ -1115,8 +1154,10 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
         for (int kk = 0; kk < kQGI; ++kk) {
             const int bk = kQRunI * half - 2 + kk;
             const int y = py0 + 2 * bi, x = px0 + 2 * bk;
-            // blocks below the frame / the buffer (a band's ragged last tile): weight 0
-            const bool inside = y + 1 < a.H && y + 1 < a.buf_y0 + a.buf_rows;
+            // blocks outside the frame / the buffer: weight 0 (interior tiles: only a band's ragged
+            // last tile has them, below the rows the merge keeps)
+            const bool inside = y + 1 < a.H && y + 1 < a.buf_y0 + a.buf_rows &&
+                                (!BRD || (y >= 0 && y >= a.buf_y0 && x >= 0 && x + 1 < a.W));
             const int64_t r = (int64_t)(y - a.buf_y0);
             const uint8_t *m0 = a.mask.p + r * a.mask.pitch + x;
             const int q = !inside ? 0 : m0[1] ? 1 : m0[a.mask.pitch] ? 2 : m0[a.mask.pitch + 1] ? 3 : 0;
@@ -1131,8 +1172,9 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
             constexpr int P = decltype(Pc)::value;
             const unsigned hs = hbase + (unsigned)P * kIStageBytes;
             int rv[kQGI];
-            for (int k = P; k < nA; k += 2) {
-                {
+            for (int k = P; k < NE; k += 2) {
+                const bool npx_entry = BRD && k == nA;                  // t = 1 per measured block
+                if (!npx_entry) {
                     const int pk = clist[k];
                     const char *bwc = reinterpret_cast<const char *>(
                         Bw + (((int)(int8_t)(pk & 0xff) - alo) >> 1) * bpitch + (int)(int8_t)((pk >> 8) & 0xff));
@@ -1147,7 +1189,7 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
                 unsigned u[kQGI], g[kQGI], m[kQGI - 1], hc = 0, hd = 0;
 #pragma unroll
                 for (int kk = 0; kk < kQGI; ++kk) {
-                    const unsigned t = __usad((unsigned)cv[kk], (unsigned)rv[kk], 0u);   // |c - r|
+                    const unsigned t = npx_entry ? 1u : __usad((unsigned)cv[kk], (unsigned)rv[kk], 0u);   // |c - r|
                     u[kk] = t * W[kk];
                     g[kk] = t * Wd[kk];
                     if (kk > 0) m[kk - 1] = g[kk - 1] + (u[kk] - g[kk]);   // D(k-1) = G_dx1(k-1) + G_dx0(k)
@@ -1162,10 +1204,11 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
                 }
                 nb_arrive_i<1 + P, kQBarI>();                           // FULL[P]
             }
-            if (P < nA) nb_sync_i<5 + P, kQBarI>();                    // drain
+            if (P < NE) nb_sync_i<5 + P, kQBarI>();                    // drain
         };
         if (pair == 0) run(std::integral_constant<int, 0>{});
         else run(std::integral_constant<int, 1>{});
+        if (BRD) asm volatile("setmaxnreg.dec.sync.aligned.u32 128;" ::: "memory");
     } else {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
         const int j = lane;
@@ -1174,7 +1217,8 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
 #pragma unroll
         for (int r = 0; r < kQSeg; ++r) { gmin[r] = 0xffffffffu; best[r] = 0xffffffffu; bestg[r] = 0u; }
         const unsigned cbase = (unsigned)__cvta_generic_to_shared(Hi + pl * kIPlane + i0 * kIPitch + j);
-        auto consume = [&](int k, auto Pc) {
+        // one ring entry: E pairs (8 E + pos) per output row pair, handed to f (r, e)
+        auto entry = [&](auto Pc, unsigned pos2, auto f) {
             constexpr int P = decltype(Pc)::value;
             nb_sync_i<1 + P, kQBarI>();                                 // FULL[P]
             const unsigned cs = cbase + (unsigned)P * kIStageBytes;
@@ -1183,15 +1227,16 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
             for (int t = 0; t < kQSeg + 4; ++t)
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x[t]) : "r"(cs + 4u * t * kIPitch) : "memory");
             nb_arrive_i<5 + P, kQBarI>();                               // EMPTY[P]
-            const unsigned pos2 = (unsigned)(k & 7) * 0x10001u;
             unsigned v = x[0] + x[1] + x[2] + x[3];
 #pragma unroll
             for (int r = 0; r < kQSeg; ++r) {
                 const unsigned vn = v + x[r + 4] - x[r];                // V(r + 1)
-                const unsigned e = v + __byte_perm(v, vn, 0x5432) + pos2;   // (8 E(2i) + pos, 8 E(2i+1) + pos)
-                gmin[r] = __vminu2(gmin[r], e);
+                f(r, v + __byte_perm(v, vn, 0x5432) + pos2);            // (8 E(2i) + pos, 8 E(2i+1) + pos)
                 v = vn;
             }
+        };
+        auto consume = [&](int k, auto Pc) {
+            entry(Pc, (unsigned)(k & 7) * 0x10001u, [&](int r, unsigned e) { gmin[r] = __vminu2(gmin[r], e); });
             if ((k & 7) == 7 || k == nA - 1) {
                 // group end: a lane takes the group's minimum iff its E is strictly smaller (the
                 // positions inside a group are not comparable across groups): 8 E_g + 7 < 8 E_best.
@@ -1209,6 +1254,12 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
             consume(k, std::integral_constant<int, 0>{});
             if (k + 1 < nA) consume(k + 1, std::integral_constant<int, 1>{});
         }
+        if (BRD) {
+            // the npx entry: gmin[r] <- (8 npx(2i), 8 npx(2i+1)) of the outputs
+            auto npx_f = [&](int r, unsigned e) { gmin[r] = e; };
+            if (nA & 1) entry(std::integral_constant<int, 1>{}, 0u, npx_f);
+            else entry(std::integral_constant<int, 0>{}, 0u, npx_f);
+        }
 #pragma unroll
         for (int r = 0; r < kQSeg; ++r)
 #pragma unroll
@@ -1218,11 +1269,20 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
                 if (val == 0xffffu || py < a.oy0 || py >= a.oy1 || px >= a.ox1) continue;
                 const unsigned gi = c ? bestg[r] >> 16 : bestg[r] & 0xffffu;
                 const int rank = clist[8 * gi + (val & 7u)] >> 16;
-                const unsigned long long key =
-                    ((unsigned long long)__float_as_uint((float)(val >> 3)) << 32) | (unsigned)rank;
+                unsigned long long hi;
+                if (BRD) {
+                    const unsigned npx = (c ? gmin[r] >> 16 : gmin[r] & 0xffffu) >> 3;
+                    if ((int)npx < a.min_support || px < a.ox0) continue;
+                    // the border body's mean key (merge_mean): floor(e * 2^13 / n)
+                    hi = (unsigned long long)floor((double)(val >> 3) * 8192.0 / (double)npx);
+                } else {
+                    hi = __float_as_uint((float)(val >> 3));
+                }
                 check_key(a, py, px);
-        atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0), key);
+                atomicMin(a.keys_p[ref_slot(a)] + (int64_t)(py - a.oy0) * a.key_pitch + (px - a.ox0),
+                          (hi << 32) | (unsigned)rank);
             }
+        if (BRD) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;" ::: "memory");
     }
 }
 
@@ -1263,12 +1323,22 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ Box
                 if (geom) {
                     if constexpr (EXACT && !SSD) {
                         if (a.int_body) {   // uint8 SAD: the integer body
-                            quad_interior_int(a, smem, chunk, px0, py0);
+                            quad_interior_int<false>(a, smem, chunk, px0, py0);
                             return;
                         }
                     }
                     quad_body<SSD, EXACT, false>(a, smem, chunk, px0, py0);
                     return;
+                }
+                if constexpr (EXACT && !SSD) {
+                    if (a.int_body) {
+                        // uint8 SAD border tile: phase 1 (clip-free candidates) in the integer body,
+                        // then the border body's phase 2 (round 2)
+                        quad_interior_int<true>(a, smem, chunk, px0, py0);
+                        __syncthreads();
+                        quad_body<SSD, EXACT, true>(a, smem, chunk, px0, py0, true);
+                        return;
+                    }
                 }
                 quad_body<SSD, EXACT, true>(a, smem, chunk, px0, py0);
                 if constexpr (EXACT && SSD) {   // quad phase 2 unavailable: the rest in the generic body

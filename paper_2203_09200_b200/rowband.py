@@ -47,9 +47,10 @@ class Band:
         return self.b1 - self.b0
 
 
-# me_box tiling (paper_2203_09200_b200/csrc): 56-row tiles from the first ME row (the band's first row
-# minus the 2-row NNC halo); a tile runs the slower border phases when an output it keeps has a window
-# that can leave the frame (measured on config 4: 1.75x an interior tile).
+# me_box tiling (paper_2203_09200_b200/csrc): 56-row tiles over the ME rows (the band's rows plus the
+# 2-row NNC halo), placed to minimise border tile rows; a tile runs the slower border phases when an
+# output it keeps has a window that can leave the frame or the band's buffer (config 4: ~1.75x an
+# interior tile).
 TILE_ROWS = 56
 BORDER_TILE_COST = 1.75
 # the fused epilogue (checks + PR) per output row, in the same unit (config 4: 0.66 ms per reference
@@ -57,14 +58,32 @@ BORDER_TILE_COST = 1.75
 EPILOGUE_PER_ROW = 0.0047
 
 
+def _tile_rows(lo: int, hi: int, H: int, S: int, K: int, b0: int, b1: int):
+    """The tile rows of me_box over output rows [lo, hi), placed as the library places them
+    (csrc/qs_api.cu place_tile_rows: the grid offset, lo - offset even, with the fewest border tile
+    rows, then the fewest rows): a list of (py0, is_border)."""
+    best = None
+    for off in range(lo & 1, TILE_ROWS, 2):
+        rows = (hi - lo + off + TILE_ROWS - 1) // TILE_ROWS
+        tiles = []
+        for t in range(rows):
+            py0 = lo - off + t * TILE_ROWS
+            ylast = min(py0 + TILE_ROWS, hi) - 1
+            tiles.append((py0, py0 - K // 2 - S < b0 or ylast + (K - 1 - K // 2) + S > b1 - 1))
+        key = (sum(b for _, b in tiles), rows)
+        if best is None or key < best[0]:
+            best = (key, tiles)
+    return best[1]
+
+
 def band_cost(y0: int, y1: int, H: int, S: int, K: int = 8) -> float:
-    """Estimated step time of the band [y0, y1) in interior-tile-row units: me_box tiles (from
-    the first ME row, border tiles weighted) plus the epilogue's rows."""
+    """Estimated step time of the band [y0, y1) in interior-tile-row units: me_box tiles (placed as
+    the library places them, border tiles weighted) plus the epilogue's rows."""
     lo, hi = max(0, y0 - 2), min(H, y1 + 2)
+    h = halo_rows(S, K)
+    b0, b1 = max(0, y0 - h), min(H, y1 + h)
     cost = EPILOGUE_PER_ROW * (y1 - y0)
-    for py0 in range(lo, hi, TILE_ROWS):
-        ylast = min(py0 + TILE_ROWS, hi) - 1
-        border = py0 - K // 2 - S < 0 or ylast + (K - 1 - K // 2) + S > H - 1
+    for _, border in _tile_rows(lo, hi, H, S, K, max(0, b0), min(H, b1)):
         cost += BORDER_TILE_COST if border else 1.0
     return cost
 

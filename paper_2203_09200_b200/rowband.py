@@ -16,7 +16,9 @@ so nothing else moves per frame.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from functools import lru_cache
 
+import numpy as np
 import torch
 
 
@@ -58,22 +60,21 @@ BORDER_TILE_COST = 1.75
 EPILOGUE_PER_ROW = 0.0047
 
 
-def _tile_rows(lo: int, hi: int, H: int, S: int, K: int, b0: int, b1: int):
-    """The tile rows of me_box over output rows [lo, hi), placed as the library places them
-    (csrc/qs_api.cu place_tile_rows: the grid offset, lo - offset even, with the fewest border tile
-    rows, then the fewest rows): a list of (py0, is_border)."""
-    best = None
-    for off in range(lo & 1, TILE_ROWS, 2):
-        rows = (hi - lo + off + TILE_ROWS - 1) // TILE_ROWS
-        tiles = []
-        for t in range(rows):
-            py0 = lo - off + t * TILE_ROWS
-            ylast = min(py0 + TILE_ROWS, hi) - 1
-            tiles.append((py0, py0 - K // 2 - S < b0 or ylast + (K - 1 - K // 2) + S > b1 - 1))
-        key = (sum(b for _, b in tiles), rows)
-        if best is None or key < best[0]:
-            best = (key, tiles)
-    return best[1]
+@lru_cache(maxsize=None)
+def _border_tile_rows(lo: int, hi: int, S: int, K: int, b0: int, b1: int) -> tuple[int, int]:
+    """(border tile rows, tile rows) of me_box over output rows [lo, hi), placed as the library places
+    them (csrc/qs_api.cu place_tile_rows: the grid offset, lo - offset even, with the fewest border tile
+    rows, then the fewest rows)."""
+    offs = np.arange(lo & 1, TILE_ROWS, 2)
+    rows = (hi - lo + offs + TILE_ROWS - 1) // TILE_ROWS
+    t = np.arange(int(rows.max()))
+    py0 = lo - offs[:, None] + t[None, :] * TILE_ROWS
+    ylast = np.minimum(py0 + TILE_ROWS, hi) - 1
+    valid = t[None, :] < rows[:, None]
+    border = ((py0 - K // 2 - S < b0) | (ylast + (K - 1 - K // 2) + S > b1 - 1)) & valid
+    nb = border.sum(axis=1)
+    i = int(np.lexsort((rows, nb))[0])
+    return int(nb[i]), int(rows[i])
 
 
 def band_cost(y0: int, y1: int, H: int, S: int, K: int = 8) -> float:
@@ -82,10 +83,8 @@ def band_cost(y0: int, y1: int, H: int, S: int, K: int = 8) -> float:
     lo, hi = max(0, y0 - 2), min(H, y1 + 2)
     h = halo_rows(S, K)
     b0, b1 = max(0, y0 - h), min(H, y1 + h)
-    cost = EPILOGUE_PER_ROW * (y1 - y0)
-    for _, border in _tile_rows(lo, hi, H, S, K, max(0, b0), min(H, b1)):
-        cost += BORDER_TILE_COST if border else 1.0
-    return cost
+    nb, rows = _border_tile_rows(lo, hi, S, K, b0, b1)
+    return EPILOGUE_PER_ROW * (y1 - y0) + rows + (BORDER_TILE_COST - 1.0) * nb
 
 
 def plan_bands(world: int, H: int, S: int, K: int = 8, h: int | None = None) -> list[int]:

@@ -456,7 +456,10 @@ extern "C" {
 
 const char *qs_last_error(void) { return g_err.c_str(); }
 
-const char *qs_version(void) { return "libqs 0.3 sm_100a (me_box quarter-sampling producer/consumer body + border phases, parity chunks; fused finalize-NNC-FRMC-PR epilogue; multi-reference launches)"; }
+const char *qs_version(void) {
+    return "libqs 0.4 sm_100a (me_box quarter-sampling bodies: fp32 with certified argmin, 16-bit-lane integer "
+           "for uint8 SAD; certify worklist; fused finalize-NNC-FRMC-PR epilogue; multi-reference launches)";
+}
 
 int qs_workspace_size(const qs_roi *roi, int32_t frame_w, int32_t frame_h, const qs_me_params *p, size_t *bytes) {
     Roi r;

@@ -59,11 +59,13 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
     __shared__ EpiShared S;
     constexpr int KL = kFK / 2;
     const int tx0 = blockIdx.x * kFT, ty0 = g.lo + blockIdx.y * kFT;
-    const tile::Regions R = tile::layout(sm, ty0, tx0, 7, g.S, g.W, g.H);
+    tile::Regions R = tile::layout(sm, ty0, tx0, 7, g.S, g.W, g.H);
     const int tid = threadIdx.x;
     const int zr = blockIdx.z;                   // reference slot (qs_me_search_refs)
     const unsigned long long *keys = g.keys_p[zr];
-    tile::stage<F32>(R, g.cur, g.mask, Plane{g.ref_p[zr], g.ref.pitch}, g.W, g.H, g.buf_y0, g.buf_rows);
+    __shared__ int box[4];                       // min / max of ly + alpha, lx + beta over valid own entries
+    if (tid < 4) box[tid] = (tid & 1) ? -(1 << 20) : (1 << 20);
+    tile::stage_cur(R, g.cur, g.mask, g.W, g.H, g.buf_y0, g.buf_rows);   // ends with __syncthreads
 
     // 1. Decode the vectors of the tile + 2-pixel halo from the keys; validity needs the
     //    support n of the chosen vector (min_support, R6), counted from the mask bits.
@@ -112,9 +114,21 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
             const int o = (r - 2) * kFT + (c - 2);
             S.st[o] = st0;
             S.n0[o] = nn;
+            if (valid) {   // the reference rows / columns this entry's window reads
+                atomicMin(&box[0], (r - 2) + va);
+                atomicMax(&box[1], (r - 2) + va);
+                atomicMin(&box[2], (c - 2) + vb);
+                atomicMax(&box[3], (c - 2) + vb);
+            }
         }
     }
     __syncthreads();
+    // Stage only the reference rows / columns the tile's vectors reach (the re-sum and FRMC read the
+    // window at p + v; round 1 staged the whole (16 + 2S + 7)^2 search region).
+    if (box[0] <= box[1]) {
+        tile::narrow_ref(R, ty0, tx0, box[0], box[1], box[2], box[3]);
+        tile::stage_ref<F32>(R, Plane{g.ref_p[zr], g.ref.pitch}, g.W, g.H, g.buf_y0, g.buf_rows);
+    }
 
     // 2. Filtered field (Eq. 1) on the tile + 1-pixel halo.
     if (NNC) {

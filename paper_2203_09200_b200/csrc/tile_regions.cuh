@@ -94,6 +94,66 @@ __device__ __forceinline__ Regions layout(float *sm, int ty0, int tx0, int maxd,
     return g;
 }
 
+// Stage the current region (NaN outside the frame / the buffer window / unmeasured) and its mask
+// bits.  One warp per region row, 32 columns per step: no index division, and the mask word of each
+// 32 columns is the warp's ballot.  Ends with __syncthreads().
+__device__ __forceinline__ void stage_cur(const Regions &g, const Plane &cur, const Plane &mask, int W, int H,
+                                          int buf_y0, int buf_rows) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const float nan = __int_as_float(0x7fc00000);
+    for (int r = warp; r < g.CR; r += nw) {
+        const int gy = g.cy0 + r;
+        const bool row_ok = gy >= 0 && gy < H && gy >= buf_y0 && gy < buf_y0 + buf_rows;
+        const int64_t rr = gy - buf_y0;
+        for (int w = 0; w < g.mwords; ++w) {
+            const int c = 32 * w + lane, gx = g.cx0 + c;
+            bool meas = false;
+            float v = nan;
+            if (row_ok && c < g.CC && gx >= 0 && gx < W && mask.p[rr * mask.pitch + gx]) {
+                meas = true;
+                v = (float)cur.p[rr * cur.pitch + gx];
+            }
+            if (c < g.cpitch) g.Cs[r * g.cpitch + c] = v;
+            const unsigned word = __ballot_sync(0xffffffffu, meas);
+            if (lane == 0) g.Mb[r * g.mwords + w] = word;
+        }
+    }
+    __syncthreads();
+}
+
+// Narrow the reference region to the rows / columns the tile's vectors reach (round 2): entries at
+// tile-local (ly, lx) with vector (a, b) read reference rows ty0 + ly + a - 4 .. + 3; lo_y / hi_y are
+// the min / max of ly + a over the tile's valid entries (likewise columns).  The region keeps its
+// base and maximum footprint (the mask bits follow it), only its origin, extent and pitch shrink.
+__device__ __forceinline__ void narrow_ref(Regions &g, int ty0, int tx0, int lo_y, int hi_y, int lo_x, int hi_x) {
+    constexpr int KL = kFK / 2;
+    g.ry0 = ty0 + lo_y - KL;
+    g.rx0 = tx0 + lo_x - KL;
+    g.RR = hi_y - lo_y + kFK;
+    g.RC = hi_x - lo_x + kFK;
+    g.rpitch = g.RC + 1;
+}
+
+// Stage the reference region (NaN outside the frame / the buffer window).  Ends with __syncthreads().
+template <bool F32>
+__device__ __forceinline__ void stage_ref(const Regions &g, const Plane &ref, int W, int H, int buf_y0, int buf_rows) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const float nan = __int_as_float(0x7fc00000);
+    for (int r = warp; r < g.RR; r += nw) {
+        const int gy = g.ry0 + r;
+        const bool row_ok = gy >= 0 && gy < H && gy >= buf_y0 && gy < buf_y0 + buf_rows;
+        const int64_t rr = gy - buf_y0;
+        for (int c = lane; c < g.rpitch; c += 32) {
+            const int gx = g.rx0 + c;
+            float v = nan;
+            if (row_ok && c < g.RC && gx >= 0 && gx < W)
+                v = F32 ? reinterpret_cast<const float *>(ref.p + rr * ref.pitch)[gx] : (float)ref.p[rr * ref.pitch + gx];
+            g.Rs[r * g.rpitch + c] = v;
+        }
+    }
+    __syncthreads();
+}
+
 // Stage both regions (NaN outside the frame / the buffer window / unmeasured) and the
 // current mask bits.  One warp per region row, 32 columns per step: no index division, and the
 // mask word of each 32 columns is the warp's ballot.  Ends with __syncthreads().

@@ -20,18 +20,23 @@ constexpr int kH2 = kFT + 4;   // decoded window: tile + 2-pixel halo (NNC's vec
 constexpr int kH1 = kFT + 2;   // filtered window: tile + 1-pixel halo
 constexpr int kCW = kFT + 14;  // FRMC window positions per axis (tile + the paper offsets' +-7)
 
-__device__ __forceinline__ int lower_median9(int (&v)[9], int n) {
-    // 25-comparator sorting network for 9 inputs (verified on all 2^9 0/1 inputs: 0-1 principle)
+// Lower median of the valid values among v[0..8] (Eq. 1, R14: invalid entries carry +1000 and sort
+// last): sort ascending with the 25-comparator network for 9 inputs (verified on all 2^9 0/1 inputs:
+// 0-1 principle), take index (n-1)/2.  Both components at once: (alpha, beta) as two signed 16-bit
+// lanes of one word, min / max per lane (VIMNMX.S16x2), so one sort serves the two medians.
+constexpr unsigned kMedSentinel = 1000u | (1000u << 16);   // invalid entries: +1000 in both lanes, sort last
+__device__ __forceinline__ unsigned pack_ab(int a, int b) { return (unsigned)(a & 0xffff) | ((unsigned)b << 16); }
+__device__ __forceinline__ unsigned lower_median9_x2(unsigned (&v)[9], int n) {
     constexpr int kNet[25][2] = {{0, 1}, {3, 4}, {6, 7}, {1, 2}, {4, 5}, {7, 8}, {0, 1}, {3, 4}, {6, 7},
                                  {0, 3}, {3, 6}, {0, 3}, {1, 4}, {4, 7}, {1, 4}, {2, 5}, {5, 8}, {2, 5},
                                  {1, 3}, {5, 7}, {2, 6}, {4, 6}, {2, 4}, {2, 3}, {5, 6}};
 #pragma unroll
     for (int c = 0; c < 25; ++c) {
-        const int a = v[kNet[c][0]], b = v[kNet[c][1]];
-        v[kNet[c][0]] = min(a, b);
-        v[kNet[c][1]] = max(a, b);
+        const unsigned a = v[kNet[c][0]], b = v[kNet[c][1]];
+        v[kNet[c][0]] = __vmins2(a, b);
+        v[kNet[c][1]] = __vmaxs2(a, b);
     }
-    int r = v[0];
+    unsigned r = v[0];
 #pragma unroll
     for (int i = 1; i < 9; ++i)
         if (i == (n - 1) / 2) r = v[i];
@@ -41,6 +46,7 @@ __device__ __forceinline__ int lower_median9(int (&v)[9], int n) {
 struct EpiShared {
     int8_t sa[kH2][kH2], sb[kH2][kH2];
     uint8_t sv[kH2][kH2];
+    unsigned sp[kH2][kH2];    // pack_ab(alpha, beta) of valid entries, kMedSentinel otherwise
     int fa[kH1][kH1], fb[kH1][kH1];
     uint8_t st[kFT * kFT];
     float m0[kFT * kFT];
@@ -84,12 +90,10 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
                 if (key != ~0ull) {
                     const int pk = __ldg(g.canon + (int)(key & 0xffffffffu));
                     const int a = (int)(int8_t)(pk & 0xff), b = (int)(int8_t)((pk >> 8) & 0xff);
-                    uint32_t colm = 0;
-#pragma unroll
-                    for (int j = 0; j < kFK; ++j) {
-                        const int qx = gx - KL + j;
-                        colm |= (qx >= 0 && qx < g.W && qx + b >= 0 && qx + b < g.W) ? (1u << j) : 0u;
-                    }
+                    // window columns qx = gx - KL + j with qx and qx + b in the frame, as a bit range
+                    const int clo = min(max(max(0, -b) - (gx - KL), 0), kFK);
+                    const int chi = min(max(min(g.W, g.W - b) - (gx - KL), 0), kFK);
+                    const uint32_t colm = (0xffu >> (kFK - chi)) & (0xffu << clo) & 0xffu;
                     int n = 0;
 #pragma unroll
                     for (int oy = 0; oy < kFK; ++oy) {
@@ -110,6 +114,7 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
         S.sa[r][c] = va;
         S.sb[r][c] = vb;
         S.sv[r][c] = valid;
+        S.sp[r][c] = valid ? pack_ab(va, vb) : kMedSentinel;
         if (r >= 2 && r < kFT + 2 && c >= 2 && c < kFT + 2) {
             const int o = (r - 2) * kFT + (c - 2);
             S.st[o] = st0;
@@ -134,21 +139,21 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
     if (NNC) {
         for (int i = tid; i < kH1 * kH1; i += blockDim.x) {
             const int r = i / kH1 + 1, c = i % kH1 + 1;
-            int la[9], lb[9], n = 0;
+            unsigned lv[9];
+            int n = 0;
 #pragma unroll
             for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
                 for (int dx = -1; dx <= 1; ++dx) {
                     const int k = (dy + 1) * 3 + (dx + 1);
-                    const bool ok = S.sv[r + dy][c + dx];
-                    la[k] = ok ? S.sa[r + dy][c + dx] : 1000;
-                    lb[k] = ok ? S.sb[r + dy][c + dx] : 1000;
-                    n += ok;
+                    lv[k] = S.sp[r + dy][c + dx];
+                    n += lv[k] != kMedSentinel;
                 }
             int ma = 0, mb = 0;
             if (S.sv[r][c]) {
-                ma = lower_median9(la, n);
-                mb = lower_median9(lb, n);
+                const unsigned m = lower_median9_x2(lv, n);
+                ma = (int)(int16_t)(m & 0xffffu);
+                mb = (int)(int16_t)(m >> 16);
             }
             S.fa[r - 1][c - 1] = ma;
             S.fb[r - 1][c - 1] = mb;
@@ -280,8 +285,9 @@ __global__ void __launch_bounds__(256, 4) epilogue_kernel(const EpiArgs g) {
     const int ne = S.n_ent;
     const int items = ne * 7;
     // delta_y-major: later rounds skip entries an earlier delta_y row already rejected.
-    for (int it = tid; it < items; it += blockDim.x) {
-        const int iy = it / ne, e = it - iy * ne;
+    int iy = ne ? tid / ne : 0, e = ne ? tid - iy * ne : 0;   // item it = iy * ne + e, one division
+    for (int it = tid; it < items; it += blockDim.x, e += blockDim.x) {
+        while (e >= ne) { e -= ne; ++iy; }
         const int o = S.ent[e];
         if (S.rej[o]) continue;
         const int ely = o / kFT, elx = o % kFT;

@@ -229,9 +229,10 @@ __device__ __forceinline__ bool frmc_item(const Regions &g, int ty0, int tx0, in
     const int rrow = (ty0 + ly + va - KL) - g.ry0, rcol = (tx0 + lx + vb - KL) - g.rx0;
     // Reference-window validity: columns x+o in the frame (a property of the entry), rows below.
     const int xx = g.rx0 + rcol, xy = g.ry0 + rrow;   // global coords of the window's (0, 0)
-    uint32_t colm = 0;
-#pragma unroll
-    for (int j = 0; j < kFK; ++j) colm |= (xx + j >= 0 && xx + j < g.W) ? (1u << j) : 0u;
+    // bits j with 0 <= xx + j < W: the in-frame column range as a mask
+    const int clo = min(max(-xx, 0), kFK), chi = min(max(g.W - xx, 0), kFK);
+    const uint32_t colm = (0xffu >> (kFK - chi)) & (0xffu << clo) & 0xffu;
+    static_assert(kFK == 8, "8-bit column masks");
     // 1. Supports n'(delta) (R6, R9): slots holding a term.
     if (cnt8 && colm == 0xffu && xy >= 0 && xy + kFK <= g.H) {
 #pragma unroll

@@ -42,6 +42,10 @@ SM_MAX_MHZ = 1965.0              # clocks.max.sm (B200_PROFILING.md)
 # H 2 + V 2 + argmin 2), is reported beside it as roofline.alt.
 OPS_PER_UNIT = 4
 OPS_PER_UNIT_DESIGN = 8
+# uint8 configs ("bound by the integer ALU pipes"): the integer-ALU peak, measured
+# per-SM issue rate of the ALU-pipe integer ops the K1i body uses (LOP3 / PRMT / VABSDIFF4 / VIMNMX,
+# MEASURED_PEAKS_INT.json: 63.3 lanes per clock per SM) x 148 SMs x the max SM clock.
+INT_ALU_LANES_PER_SM = 63.3
 
 
 def parse():
@@ -280,8 +284,10 @@ def run_ours(args):
     rechecked = qs.qs_certify_stats(reset=True)
     ms = t0.elapsed_time(t1)
     prof = {k: qs.qs_profile_read(k) for k in qs.PROFILE_KERNELS}
-    # kernels launched in the timed region: one per qs_profile scope, two for certify (scan + fix)
-    launches = sum(n for _, n in prof.values()) + prof["certify"][1]
+    # kernels launched in the timed region: one per qs_profile scope, two for certify (scan + fix) and,
+    # for float references, two for me_box (border and interior grids; QS_SPLIT=0 selects one kernel)
+    split = f32 and K == 8 and os.environ.get("QS_SPLIT", "1") != "0"
+    launches = sum(n for _, n in prof.values()) + prof["certify"][1] + (prof["me_box"][1] if split else 0)
     conc = None
     if cmp_mode:
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -326,6 +332,15 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # SURVEY.md 8(d.4)'s primary "pipe roofline": the busiest pipes' active fraction of me_box, from the
+    # committed ncu --set full capture of this config (profiles/me_box_pipes_c<cfg>.json; None if absent).
+    pipes = None
+    ppath = os.path.join(ROOT, "profiles", f"me_box_pipes_c{args.config}.json")
+    if os.path.exists(ppath):
+        try:
+            pipes = json.load(open(ppath))
+        except Exception:
+            pipes = None
     alt = OPS_PER_UNIT_DESIGN * units_per_launch / (me_ms / me_n / 1e3) / 1e12 if me_n else None
     roofline = {"bound": "alu", "kernel": "me_box", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
@@ -335,7 +350,13 @@ def run_ours(args):
                 "share_of_step": me_ms / ms if ms else None,
                 "alt": {"ops_per_unit": OPS_PER_UNIT_DESIGN, "achieved": alt,
                         "frac": (alt / peak) if alt else None, "basis": "DESIGN.md section 6 per-stage count"},
-                "peak_basis": "148 SM x 128 FP32 lanes x 1965 MHz (guide unit counts and max clock)"}
+                "peak_basis": "148 SM x 128 FP32 lanes x 1965 MHz (guide unit counts and max clock)",
+                "pipe": pipes}
+    if not f32 and achieved:
+        ipk = SM_COUNT * INT_ALU_LANES_PER_SM * SM_MAX_MHZ * 1e6 / 1e12
+        roofline["int_alu"] = {"peak": ipk, "unit": "T int op/s", "frac": achieved / ipk,
+                               "basis": "same 4 ops per (pixel, candidate) against the integer-ALU pipe peak "
+                                        "(SURVEY.md 8(d.4) sanity ceiling; MEASURED_PEAKS_INT.json)"}
     kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
 
     e2e = None

@@ -25,6 +25,7 @@
 // rows) forms E and updates the running best.  Chunks of the same tile merge
 // with a 64-bit atomicMin on (order key << 32 | rank), which is exact because
 // the order key is monotone in the mean and equal means give equal keys.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <type_traits>
@@ -66,6 +67,15 @@ __device__ __forceinline__ float fkey(float v, unsigned k) {
 __device__ __forceinline__ void fbest(float &m1, float &m2, float key) {
     m2 = fminf(m2, fmaxf(m1, key));
     m1 = fminf(m1, key);
+}
+// The same on the keys' bits as unsigned integers (RUNS phase 2): a negative value (an inadmissible
+// candidate, coded e * (-1)) has the sign bit set and orders after every non-negative key.
+__device__ __forceinline__ void ubest(float &m1, float &m2, unsigned key) {
+    unsigned x = __float_as_uint(m1), y = __float_as_uint(m2);
+    y = min(y, max(x, key));
+    x = min(x, key);
+    m1 = __uint_as_float(x);
+    m2 = __uint_as_float(y);
 }
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
@@ -496,10 +506,15 @@ constexpr int kQPlanes = 4;   // planes per ring stage
 __host__ __device__ constexpr int quad_pitch(int cols) { return 2 * (((cols + 1) / 2) | 1); }
 __host__ __device__ constexpr int quad_plane(int rows, int cols) { return (((rows + 1) / 2) * quad_pitch(cols) + 31) & ~31; }
 
-template <bool SSD, bool EXACT, bool BORDER>
+// RUNS (float border tiles of a split launch): phase 2 in runs of equal supports -- the list-B
+// candidates sorted by their support key (the support planes depend on v only through the rows /
+// columns that clip), the producers roll the support planes once per run and the consumers keep
+// 1 / n per output for the run.
+template <bool SSD, bool EXACT, bool BORDER, bool RUNS = false>
 __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chunk, int px0, int py0,
                                           bool skip_phase1 = false) {
     constexpr bool Q2 = BORDER && !(EXACT && SSD);
+    static_assert(!RUNS || (BORDER && !EXACT), "support runs: float border tiles only");
     const int alo = chunk_alo(a.S, chunk);
     const int ahi = chunk_ahi(a.S, chunk);
     const int nrow_b = kQWinRows + (ahi - alo);
@@ -597,6 +612,50 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 }
                 if (lane == 0) nsel[pass] = n;
             }
+        }
+        if constexpr (RUNS) {
+            // Support key of each list-B candidate: (alpha if its rows clip, beta if its columns clip);
+            // equal keys = identical support planes.  Sorted (rank order inside a key) by counting the
+            // entries before each one; order inside the list is free for the float argmin (the keyed
+            // position decodes the rank; near-ties are recomputed exactly by certify).
+            __syncthreads();
+            const int b0 = nsel[0], nb = nsel[1] - nsel[0];
+            int *skey = nsel + 8, *stmp = skey + kChunkRows * (2 * a.S + 1);
+            const int qy_lo = max(0, py0 - 4), qy_hi = min(a.H - 1, py0 + kTY + 2);
+            const int qx_lo = max(0, px0 - 4), qx_hi = min(a.W - 1, px0 + kTX + 2);
+            for (int i = threadIdx.x; i < nb; i += kNT) {
+                const int pk = clist[b0 + i];
+                const int al = (int)(int8_t)(pk & 0xff), bt = (int)(int8_t)((pk >> 8) & 0xff);
+                const bool rc = qy_lo + al < 0 || qy_hi + al > a.H - 1;
+                const bool cc = qx_lo + bt < 0 || qx_hi + bt > a.W - 1;
+                stmp[i] = ((rc ? al + 64 : 0) << 8) | (cc ? bt + 64 : 0);
+            }
+            __syncthreads();
+            int dst[2], pks[2], ks[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int i = threadIdx.x + u * kNT;
+                dst[u] = -1;
+                if (i < nb) {
+                    const int ki = stmp[i];
+                    int d = 0;
+                    for (int jx = 0; jx < nb; ++jx) {
+                        const int kj = stmp[jx];
+                        d += (kj < ki || (kj == ki && jx < i)) ? 1 : 0;
+                    }
+                    dst[u] = d;
+                    pks[u] = clist[b0 + i];
+                    ks[u] = ki;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (dst[u] >= 0) {
+                    clist[b0 + dst[u]] = pks[u];
+                    skey[dst[u]] = ks[u];
+                }
+            static_assert(2 * kNT >= kChunkRows * 65, "two list-B entries per thread cover S <= 32");
         }
     }
     __syncthreads();
@@ -775,6 +834,8 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
     if (warp < 4) {
         // ------------------------------ producer ------------------------------
         // lane = H row (block row + 2), 8 H columns per warp, 12 blocks read per lane.
+        // RUNS: registers move to the consumers (their 1 / n per output): producers 120, consumers 136.
+        if constexpr (RUNS) asm volatile("setmaxnreg.dec.sync.aligned.u32 120;" ::: "memory");
         const int hr = lane;
         const int bi = hr - 2;
         float cv[kQG], wx[kQG];
@@ -838,7 +899,13 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         // One ring entry e in stage s: reduce the candidate whose gathers are in cur[] while the
         // gathers of list position nci go to nxt[] (nci < 0: none).  mode 0: phase-1 candidate,
         // 1: the npx entry (d = 1 per measured pixel), 2: phase-2 candidate (+ support planes).
-        auto produce = [&](int e, const int s, const float (&cur)[kQG], float (&nxt)[kQG], int nci, const int mode) {
+        auto produce = [&](int e, const int s, const float (&cur)[kQG], float (&nxt)[kQG], int nci, const int mode,
+                           int ci = 0) {
+            bool roll_n = true;   // support planes of this entry (RUNS: only at a run's first entry)
+            if constexpr (RUNS) {
+                const int* skey = nsel + 8;
+                roll_n = ci == a0 || skey[ci - a0] != skey[ci - a0 - 1];
+            }
             if (nci >= 0) gather(nci, nxt);
             if (e >= kQStages) nb_sync(5 + s, kNT);                  // EMPTY[s]: consumers released stage s
             const unsigned hs = hbase + (unsigned)s * kStageBytes;
@@ -851,7 +918,13 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                 const float t0 = SSD ? __fmul_rn(d, d) : fabsf(d);
                 const float t = fmaxf(t0, 0.f);                       // NaN (outside the frame) -> 0
                 roll(R, kk, t, hs, 0);
-                if (Q2 && mode == 2) roll(N, kk, (t0 == t0) ? 1.f : 0.f, hs, 2);   // term indicator
+                if (!RUNS && Q2 && mode == 2) roll(N, kk, (t0 == t0) ? 1.f : 0.f, hs, 2);   // term indicator
+            }
+            if constexpr (RUNS) {   // support planes at a run's first entry only, in a loop of their own
+                if (mode == 2 && roll_n) {
+#pragma unroll
+                    for (int kk = 0; kk < kQG; ++kk) roll(N, kk, (cur[kk] == cur[kk]) ? 1.f : 0.f, hs, 2);
+                }
             }
             nb_arrive(1 + s, kNT);                                   // FULL[s]
         };
@@ -863,13 +936,13 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
             gather(ci0, ra);
             if ((e0 & 1) == 0) {
                 for (int i = 0; i < n; i += 2) {
-                    produce(e0 + i, 0, ra, rb, i + 1 < n ? ci0 + i + 1 : -1, mode);
-                    if (i + 1 < n) produce(e0 + i + 1, 1, rb, ra, i + 2 < n ? ci0 + i + 2 : -1, mode);
+                    produce(e0 + i, 0, ra, rb, i + 1 < n ? ci0 + i + 1 : -1, mode, ci0 + i);
+                    if (i + 1 < n) produce(e0 + i + 1, 1, rb, ra, i + 2 < n ? ci0 + i + 2 : -1, mode, ci0 + i + 1);
                 }
             } else {
                 for (int i = 0; i < n; i += 2) {
-                    produce(e0 + i, 1, ra, rb, i + 1 < n ? ci0 + i + 1 : -1, mode);
-                    if (i + 1 < n) produce(e0 + i + 1, 0, rb, ra, i + 2 < n ? ci0 + i + 2 : -1, mode);
+                    produce(e0 + i, 1, ra, rb, i + 1 < n ? ci0 + i + 1 : -1, mode, ci0 + i);
+                    if (i + 1 < n) produce(e0 + i + 1, 0, rb, ra, i + 2 < n ? ci0 + i + 2 : -1, mode, ci0 + i + 1);
                 }
             }
         };
@@ -885,6 +958,7 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
         // ------------------------------ consumer ------------------------------
         // lane = block column j; plane pl (0: C, output column 2j; 1: D, output column 2j+1);
         // block rows i0 .. i0+13, both row parities; candidates in rank order, strict '<' (R7).
+        if constexpr (RUNS) asm volatile("setmaxnreg.inc.sync.aligned.u32 136;" ::: "memory");
         const int j = lane;
         const int cw = warp - 4, pl = cw & 1, i0 = kQSeg * (cw >> 1);
         // exact (uint8): best (e, rank) / (e, n, rank); float (FK): be / m2 = the two smallest keyed
@@ -1038,15 +1112,71 @@ __device__ __forceinline__ void quad_body(const BoxArgs &a, float *smem, int chu
                         }
                     }
                 };
+                // RUNS: 1 / n of the current support run per output (negative: n < min_support).
+                float rn[RUNS ? kQSeg : 1][2];
+                auto consume2r = [&](int ci, const int s) {
+                    const int *skey = nsel + 8;
+                    const bool rstart = ci == a0 || skey[ci - a0] != skey[ci - a0 - 1];
+                    nb_sync(1 + s, kNT);                                 // FULL[s]
+                    const unsigned cs = cbase + (unsigned)s * kStageBytes, ns = cs + 2u * kPlane * 8u;
+                    if (rstart) {   // the run's supports: vertical boxes of the support planes
+                        f2_t y0 = ld_shared_f2(ns), y1 = ld_shared_f2(ns + 8 * kQHP), y2 = ld_shared_f2(ns + 16 * kQHP);
+                        f2_t y3 = ld_shared_f2(ns + 24 * kQHP), yl = ld_shared_f2(ns + 32 * kQHP);
+                        f2_t qq0 = f2add(y0, y1), qq1 = f2add(y1, y2), qq2 = f2add(y2, y3), qq3 = f2add(y3, yl);
+                        f2_t ncur = f2add(qq0, qq2);
+#pragma unroll
+                        for (int r = 0; r < kQSeg; ++r) {
+                            const f2_t nnext = f2add(qq1, qq3);
+                            const float nv[2] = {__fadd_rn(f2lo(ncur), f2hi(ncur)), __fadd_rn(f2hi(ncur), f2lo(nnext))};
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) rn[r][c] = nv[c] >= ms ? rcp_approx(nv[c]) : -1.f;
+                            ncur = nnext;
+                            qq0 = qq1;
+                            qq1 = qq2;
+                            qq2 = qq3;
+                            if (r + 5 < kQSeg + 4) {
+                                const f2_t yn = ld_shared_f2(ns + 8 * (r + 5) * kQHP);
+                                qq3 = f2add(yl, yn);
+                                yl = yn;
+                            }
+                        }
+                    }
+                    f2_t x0 = ld_shared_f2(cs), x1 = ld_shared_f2(cs + 8 * kQHP), x2 = ld_shared_f2(cs + 16 * kQHP);
+                    f2_t x3 = ld_shared_f2(cs + 24 * kQHP), xl = ld_shared_f2(cs + 32 * kQHP);
+                    f2_t pp0 = f2add(x0, x1), pp1 = f2add(x1, x2), pp2 = f2add(x2, x3), pp3 = f2add(x3, xl);
+                    f2_t vcur = f2add(pp0, pp2);
+#pragma unroll
+                    for (int r = 0; r < kQSeg; ++r) {
+                        const f2_t vnext = f2add(pp1, pp3);
+                        const float ev[2] = {__fadd_rn(f2lo(vcur), f2hi(vcur)), __fadd_rn(f2hi(vcur), f2lo(vnext))};
+#pragma unroll
+                        for (int c = 0; c < 2; ++c)
+                            ubest(be[r][c], m2[r][c], __float_as_uint(fkey(__fmul_rn(ev[c], rn[r][c]), (unsigned)ci)));
+                        vcur = vnext;
+                        pp0 = pp1;
+                        pp1 = pp2;
+                        pp2 = pp3;
+                        if (r + 5 < kQSeg + 4) {
+                            const f2_t xn = ld_shared_f2(cs + 8 * (r + 5) * kQHP);
+                            pp3 = f2add(xl, xn);
+                            xl = xn;
+                            if (r + 5 == kQSeg + 3) nb_arrive(5 + s, kNT);   // EMPTY[s]: last rows read
+                        }
+                    }
+                };
+                auto c2 = [&](int ci, const int st) {
+                    if constexpr (RUNS) consume2r(ci, st);
+                    else consume2(ci, st);
+                };
                 if ((e1 & 1) == 0) {
                     for (int i = 0; i < nB; i += 2) {
-                        consume2(a0 + i, 0);
-                        if (i + 1 < nB) consume2(a0 + i + 1, 1);
+                        c2(a0 + i, 0);
+                        if (i + 1 < nB) c2(a0 + i + 1, 1);
                     }
                 } else {
                     for (int i = 0; i < nB; i += 2) {
-                        consume2(a0 + i, 1);
-                        if (i + 1 < nB) consume2(a0 + i + 1, 0);
+                        c2(a0 + i, 1);
+                        if (i + 1 < nB) c2(a0 + i + 1, 0);
                     }
                 }
 #pragma unroll
@@ -1286,17 +1416,55 @@ __device__ __forceinline__ void quad_interior_int(const BoxArgs &a, float *smem,
     }
 }
 
-template <int K, bool EXACT, bool SSD, bool REV>
+// TILES (K = 8 forward launches): 0 = every tile; 1 = interior tiles only; 2 = border tiles only (a
+// separate kernel so each class gets its own code generation; the interior launch follows the border
+// launch as a programmatic dependent launch, launch_t).
+template <bool ON>
+struct PdlWaitAtExit {   // the interior grid of a split launch completes only after the border grid
+    __device__ ~PdlWaitAtExit() {
+        if constexpr (ON) asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+};
+
+template <int K, bool EXACT, bool SSD, bool REV, int TILES = 0>
 __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ BoxArgs a) {
+    [[maybe_unused]] PdlWaitAtExit<TILES == 1> pdl_guard;
     extern __shared__ __align__(1024) float smem[];   // TMA box destinations need 128-byte alignment
     const int unit = blockIdx.x / a.n_ref;   // the slots of one unit run side by side
     const int chunk = unit % a.n_chunks;
     const int tile = unit / a.n_chunks;
-    const int txi = tile % a.tiles_x;
-    // Tile rows in the order first, last, second-to-last, then the rest: the (slower) frame-border
-    // rows are scheduled in the first waves, not in the tail.
-    const int q = tile / a.tiles_x, T = a.tiles_y;
-    const int tyi = T < 3 ? q : (q == 0 ? 0 : q == 1 ? T - 1 : q == 2 ? T - 2 : q - 2);
+    int txi, tyi;
+    if (TILES != 0 && a.rect_r0 < 0) {   // split launch over the whole grid (each class skips the other)
+        txi = tile % a.tiles_x;
+        const int q = tile / a.tiles_x, T = a.tiles_y;
+        tyi = T < 3 ? q : (q == 0 ? 0 : q == 1 ? T - 1 : q == 2 ? T - 2 : q - 2);
+    } else if constexpr (TILES == 1) {
+        // interior launch: the tiles of the interior rectangle [r0, r1) x [c0, c1)
+        const int nc = a.rect_c1 - a.rect_c0;
+        tyi = a.rect_r0 + tile / nc;
+        txi = a.rect_c0 + tile % nc;
+    } else if constexpr (TILES == 2) {
+        // border launch: the rows above and below the rectangle, then the columns left and right of it
+        const int tx = a.tiles_x, top = a.rect_r0 * tx, bot = (a.tiles_y - a.rect_r1) * tx;
+        if (tile < top) {
+            tyi = tile / tx;
+            txi = tile % tx;
+        } else if (tile < top + bot) {
+            tyi = a.rect_r1 + (tile - top) / tx;
+            txi = (tile - top) % tx;
+        } else {
+            const int w = a.rect_c0 + (tx - a.rect_c1), m = tile - top - bot;
+            tyi = a.rect_r0 + m / w;
+            const int k = m % w;
+            txi = k < a.rect_c0 ? k : a.rect_c1 + (k - a.rect_c0);
+        }
+    } else {
+        txi = tile % a.tiles_x;
+        // Tile rows in the order first, last, second-to-last, then the rest: the (slower) frame-border
+        // rows are scheduled in the first waves, not in the tail.
+        const int q = tile / a.tiles_x, T = a.tiles_y;
+        tyi = T < 3 ? q : (q == 0 ? 0 : q == 1 ? T - 1 : q == 2 ? T - 2 : q - 2);
+    }
     // tile_off (forward K = 8 launches): the tile grid starts tile_off rows above oy0, placed by the
     // host so that the fewest tile rows reach outside the frame (border tiles cost ~1.7x).
     const int px0 = a.ox0 + txi * kTX, py0 = a.oy0 - a.tile_off + tyi * kTY;
@@ -1307,20 +1475,30 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ Box
         box_body<K, EXACT, true, SSD, true>(a, smem, chunk, px0, py0);
     } else {
         if constexpr (K == 8) {
+            // Rows: only the outputs the merge keeps (rows < oy1) must have every window in the
+            // frame and the buffer; rows beyond (a band's ragged last tile) read NaN windows and
+            // are never merged.  Columns: the whole tile (ox1 is the frame width).
+            const int ylast = min(py0 + kTY, a.oy1) - 1;
+            const bool geom = (py0 - 4 - a.S >= 0) && (ylast + 3 + a.S <= a.H - 1) &&
+                              (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1) &&
+                              (py0 - 4 - a.S >= a.buf_y0) && (ylast + 3 + a.S < a.buf_y0 + a.buf_rows);
+            if constexpr (TILES == 2) asm volatile("griddepcontrol.launch_dependents;");
+            // the host's rectangle (launch_t) mirrors geom: interior launch = geom tiles, border = the rest
+            if constexpr (TILES == 1) {
+                if (a.rect_r0 < 0 && !geom) return;
+                QS_DCHECK(geom);
+            }
+            if constexpr (TILES == 2) {
+                if (a.rect_r0 < 0 && geom) return;
+                QS_DCHECK(!geom);
+            }
             // Quarter-sampling body.  Interior: every pixel it touches, for every candidate, lies in the
             // frame and in the caller's buffer.  Border: clip-free candidates here, the rest below.
             if (a.S >= 4 && quad_mask_ok(a, px0, py0)) {
-                // Rows: only the outputs the merge keeps (rows < oy1) must have every window in the
-                // frame and the buffer; rows beyond (a band's ragged last tile) read NaN windows and
-                // are never merged.  Columns: the whole tile (ox1 is the frame width).
-                const int ylast = min(py0 + kTY, a.oy1) - 1;
-                const bool geom = (py0 - 4 - a.S >= 0) && (ylast + 3 + a.S <= a.H - 1) &&
-                                  (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1) &&
-                                  (py0 - 4 - a.S >= a.buf_y0) && (ylast + 3 + a.S < a.buf_y0 + a.buf_rows);
 #ifdef QS_EXP_SKIP   // measurement builds only (tools/build_exp.sh): 1 = skip border tiles, 2 = skip interior
                 if ((QS_EXP_SKIP == 1 && !geom) || (QS_EXP_SKIP == 2 && geom)) return;
 #endif
-                if (geom) {
+                if (TILES != 2 && geom) {
                     if constexpr (EXACT && !SSD) {
                         if (a.int_body) {   // uint8 SAD: the integer body
                             quad_interior_int<false>(a, smem, chunk, px0, py0);
@@ -1330,6 +1508,7 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ Box
                     quad_body<SSD, EXACT, false>(a, smem, chunk, px0, py0);
                     return;
                 }
+                if constexpr (TILES == 1) return;   // unreachable: interior launch, geom tiles only
                 if constexpr (EXACT && !SSD) {
                     if (a.int_body) {
                         // uint8 SAD border tile: phase 1 (clip-free candidates) in the integer body,
@@ -1340,7 +1519,7 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ Box
                         return;
                     }
                 }
-                quad_body<SSD, EXACT, true>(a, smem, chunk, px0, py0);
+                quad_body<SSD, EXACT, true, TILES == 2 && !EXACT>(a, smem, chunk, px0, py0);
                 if constexpr (EXACT && SSD) {   // quad phase 2 unavailable: the rest in the generic body
                     __syncthreads();
                     box_body<K, EXACT, true, SSD, false>(a, smem, chunk, px0, py0, true);
@@ -1353,8 +1532,8 @@ __global__ void __launch_bounds__(kNT, 2) box_kernel(const __grid_constant__ Box
     }
 }
 
-template <int K, bool EXACT, bool SSD, bool REV>
-cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
+template <int K, bool EXACT, bool SSD, bool REV, int TILES>
+cudaError_t launch_t1(const BoxArgs &a, cudaStream_t s, bool pdl, long long tiles) {
     using G = BoxGeom<K>;
     const int nrow_b = G::HR + kChunkSpan - 1;
     const int bpitch = (kTX + K - 1 + 2 * a.S) | 1;
@@ -1364,16 +1543,84 @@ cudaError_t launch_t(const BoxArgs &a, cudaStream_t s) {
         const int qrows = kQWinRows + kChunkSpan - 1, qcols = kQWinCols + 2 * a.S;
         const size_t plane = a.tma ? (size_t)((a.tma_rows * a.tma_cols + 31) & ~31) : (size_t)quad_plane(qrows, qcols);
         const size_t qs = sizeof(float) * 2 * plane +
-                          sizeof(f2_t) * kQStages * kQPlanes * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8);
+                          sizeof(f2_t) * kQStages * kQPlanes * kQHR * kQHP + sizeof(int) * (kChunkRows * (2 * a.S + 1) + 8) +
+                          (TILES == 2 ? sizeof(int) * 2 * kChunkRows * (2 * a.S + 1) : 0);   // RUNS: keys + sort
         smem = smem > qs ? smem : qs;
     }
-    auto fn = box_kernel<K, EXACT, SSD, REV>;
+    auto fn = box_kernel<K, EXACT, SSD, REV, TILES>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const long long units = (long long)a.tiles_x * a.tiles_y * a.n_chunks * a.n_ref;
+    const long long units = tiles * a.n_chunks * a.n_ref;
     if (units <= 0) return cudaSuccess;
-    fn<<<(unsigned)units, kNT, smem, s>>>(a);
-    return cudaGetLastError();
+    if (!pdl) {
+        fn<<<(unsigned)units, kNT, smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)units);
+    cfg.blockDim = dim3(kNT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
+// Interior rectangle of a K = 8 forward launch in tile coordinates: box_kernel's geom (every window
+// of the tile's kept outputs, for every candidate, in the frame and the buffer) is a conjunction of a
+// row condition and a column condition, each true on a contiguous range of tile rows / columns.
+inline bool interior_rect(BoxArgs &a) {
+    int r0 = -1, r1 = -1, c0 = -1, c1 = -1;
+    for (int t = 0; t < a.tiles_y; ++t) {
+        const int py0 = a.oy0 - a.tile_off + t * kTY, ylast = std::min(py0 + kTY, a.oy1) - 1;
+        const bool ok = (py0 - 4 - a.S >= 0) && (ylast + 3 + a.S <= a.H - 1) && (py0 - 4 - a.S >= a.buf_y0) &&
+                        (ylast + 3 + a.S < a.buf_y0 + a.buf_rows);
+        if (ok && r0 < 0) r0 = t;
+        if (ok) r1 = t + 1;
+    }
+    for (int t = 0; t < a.tiles_x; ++t) {
+        const int px0 = a.ox0 + t * kTX;
+        const bool ok = (px0 - 4 - a.S >= 0) && (px0 + kQWinCols - 5 + a.S <= a.W - 1);
+        if (ok && c0 < 0) c0 = t;
+        if (ok) c1 = t + 1;
+    }
+    if (r0 < 0 || c0 < 0) return false;
+    a.rect_r0 = r0;
+    a.rect_r1 = r1;
+    a.rect_c0 = c0;
+    a.rect_c1 = c1;
+    return true;
+}
+
+template <int K, bool EXACT, bool SSD, bool REV>
+cudaError_t launch_t(const BoxArgs &a0, cudaStream_t s) {
+    const long long all = (long long)a0.tiles_x * a0.tiles_y;
+    if constexpr (K == 8 && !REV && !EXACT) {
+        // Float references: border tiles and interior tiles as two kernels, the
+        // border one with phase 2 in runs of equal supports.  The interior grid is a programmatic
+        // dependent launch: it starts filling SMs as the border grid's last wave drains (every border CTA
+        // triggers at its start), and each interior CTA waits for the border grid's completion before it
+        // exits, so the stream's next operation sees both grids complete.
+        BoxArgs a = a0;
+        if (a.split_tiles == 2) {   // whole grid twice, each class skipping the other's tiles
+            a.rect_r0 = -1;
+            cudaError_t e = launch_t1<K, EXACT, SSD, REV, 2>(a, s, false, all);
+            if (e != cudaSuccess) return e;
+            return launch_t1<K, EXACT, SSD, REV, 1>(a, s, true, all);
+        }
+        if (a.split_tiles && interior_rect(a)) {
+            const long long inner = (long long)(a.rect_r1 - a.rect_r0) * (a.rect_c1 - a.rect_c0);
+            if (inner < all) {
+                cudaError_t e = launch_t1<K, EXACT, SSD, REV, 2>(a, s, false, all - inner);
+                if (e != cudaSuccess) return e;
+            }
+            return launch_t1<K, EXACT, SSD, REV, 1>(a, s, inner < all, inner);
+        }
+    }
+    return launch_t1<K, EXACT, SSD, REV, 0>(a0, s, false, all);
 }
 
 template <int K>

@@ -282,6 +282,13 @@ int tma_enabled() {
     return (e && !strcmp(e, "1")) ? 1 : 0;
 }
 
+// Float-reference K = 8 forward me_box as two kernels, border tiles (phase 2 in support runs) then
+// interior tiles (default; QS_SPLIT=0 selects the single kernel for the measured comparison in DESIGN.md).
+int split_tiles_enabled() {
+    const char *e = getenv("QS_SPLIT");   // read per call (cheap), so a process can switch
+    return (e && !strcmp(e, "0")) ? 0 : (e && !strcmp(e, "2")) ? 2 : 1;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void *ptr = nullptr;
@@ -351,6 +358,7 @@ BoxArgs box_args(const Roi &r, const uint8_t *cur, const uint8_t *mask, int64_t 
                  int64_t ref_pitch, const qs_me_params *p, const CandTables *t) {
     BoxArgs a{};
     a.int_body = u8_int_body();
+    a.split_tiles = split_tiles_enabled();
     a.cur = Plane{cur, cur_pitch};
     a.mask = Plane{mask, cur_pitch};
     a.ref = Plane{static_cast<const uint8_t *>(ref), ref_pitch};

@@ -110,6 +110,10 @@ struct BoxArgs {
     // [tma_rows][1][tma_cols] (one per row-parity plane), out-of-frame / out-of-buffer elements
     // filled with NaN ("no term").  tma = 0: cp.async / register staging.
     int tma, tma_cols, tma_rows;
+    // K = 8 forward, float references: 1 = border tiles and interior tiles as two kernels (own code
+    // generation each), the interior one a programmatic dependent launch (me_box.cuh launch_t).
+    int split_tiles;
+    int rect_r0, rect_r1, rect_c0, rect_c1;   // split launches: interior tiles [r0, r1) x [c0, c1) (launch_t)
     CUtensorMap tmap[kMaxRefs];
 };
 

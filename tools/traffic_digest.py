@@ -26,9 +26,10 @@ def main():
         d = launches.setdefault(key, {"kernel": name})
         d[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
     seq = list(launches.values())
-    per_step = len(seq) // (len(seq) // max(1, sum(1 for x in seq if x["kernel"] == "box_kernel")) and 1)
-    n_box = sum(1 for x in seq if x["kernel"] == "box_kernel")
-    per_step = len(seq) // n_box
+    # one epilogue launch per step; float references launch me_box as two grids (border, interior)
+    n_epi = sum(1 for x in seq if x["kernel"] == "epilogue_kernel")
+    n_box = n_epi
+    per_step = len(seq) // n_epi
     timed = seq[-steps * per_step:]
     agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0, 0])
     for x in timed:
@@ -48,9 +49,11 @@ def main():
         out["kernels"][k] = {"launches": n, "dram_read_per_launch": rd / n, "dram_write_per_launch": wr / n,
                              "dram_bytes_per_launch": (rd + wr) / n, "duration_per_launch": t / n}
     bx = out["kernels"].get("box_kernel")
-    if bx:
-        out["dram_bytes_per_launch"] = bx["dram_bytes_per_launch"]
-        out["me_box_traffic_over_algorithmic_inputs"] = bx["dram_bytes_per_launch"] / alg_in
+    if bx:   # per me_box call (qs_me_search_refs): every box grid of one step
+        per_call = bx["dram_bytes_per_launch"] * bx["launches"] / steps
+        out["box_grids_per_call"] = bx["launches"] / steps
+        out["dram_bytes_per_launch"] = per_call
+        out["me_box_traffic_over_algorithmic_inputs"] = per_call / alg_in
     tot = sum(v["dram_bytes_per_launch"] * v["launches"] for v in out["kernels"].values()) / steps
     out["dram_bytes_per_step_all_kernels"] = tot
     out["per_step_over_algorithmic_inputs_plus_pr_planes"] = tot / (alg_in + 2 * px * esz + 5 * px)

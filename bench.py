@@ -184,8 +184,9 @@ def run_ours(args):
         band = rowband.band_of(0, 1, H, rowband.halo_rows(S, K))
         seq, frames = make_frames(args.config, args.frames, s=rank)
     else:
-        # cost-balanced row bands (rowband.plan_bands: border tiles weigh 1.75 interior tiles)
-        band = rowband.band_of(rank, world, H, rowband.halo_rows(S, K), S=S, K=K)
+        # cost-balanced row bands (rowband.plan_bands: border tiles weigh 1.75 interior tiles, 1.46 for
+        # float references)
+        band = rowband.band_of(rank, world, H, rowband.halo_rows(S, K), S=S, K=K, f32=f32)
         seq, frames = make_frames(args.config, args.frames)
     banded = world > 1 and not args.sequences
 

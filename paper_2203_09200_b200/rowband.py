@@ -51,10 +51,13 @@ class Band:
 
 # me_box tiling (paper_2203_09200_b200/csrc): 56-row tiles over the ME rows (the band's rows plus the
 # 2-row NNC halo), placed to minimise border tile rows; a tile runs the slower border phases when an
-# output it keeps has a window that can leave the frame or the band's buffer (config 4: ~1.75x an
-# interior tile).
+# output it keeps has a window that can leave the frame or the band's buffer: ~1.75x an interior tile
+# for uint8 references; float references run border tiles in a grid of their own with phase 2 in support
+# runs, measured 1.46x (config 4: 1.94 ms for 96 border tiles, 6.97 ms for
+# 504 interior tiles, profiles/r02c/ncu_box_{border,interior}_c4.json).
 TILE_ROWS = 56
 BORDER_TILE_COST = 1.75
+BORDER_TILE_COST_F32 = 1.46
 # the fused epilogue (checks + PR) per output row, in the same unit (config 4: 0.66 ms per reference
 # and frame against 0.13 ms per interior tile row and reference)
 EPILOGUE_PER_ROW = 0.0047
@@ -77,17 +80,18 @@ def _border_tile_rows(lo: int, hi: int, S: int, K: int, b0: int, b1: int) -> tup
     return int(nb[i]), int(rows[i])
 
 
-def band_cost(y0: int, y1: int, H: int, S: int, K: int = 8) -> float:
+def band_cost(y0: int, y1: int, H: int, S: int, K: int = 8, f32: bool = False) -> float:
     """Estimated step time of the band [y0, y1) in interior-tile-row units: me_box tiles (placed as
     the library places them, border tiles weighted) plus the epilogue's rows."""
     lo, hi = max(0, y0 - 2), min(H, y1 + 2)
     h = halo_rows(S, K)
     b0, b1 = max(0, y0 - h), min(H, y1 + h)
     nb, rows = _border_tile_rows(lo, hi, S, K, b0, b1)
-    return EPILOGUE_PER_ROW * (y1 - y0) + rows + (BORDER_TILE_COST - 1.0) * nb
+    w = BORDER_TILE_COST_F32 if f32 else BORDER_TILE_COST
+    return EPILOGUE_PER_ROW * (y1 - y0) + rows + (w - 1.0) * nb
 
 
-def plan_bands(world: int, H: int, S: int, K: int = 8, h: int | None = None) -> list[int]:
+def plan_bands(world: int, H: int, S: int, K: int = 8, h: int | None = None, f32: bool = False) -> list[int]:
     """Even row cuts 0 = c_0 < ... < c_world = H minimising the largest band_cost (bands at least h
     rows): the smallest cost bound T for which greedy packing covers the frame, then the cuts."""
     h = halo_rows(S, K) if h is None else h
@@ -101,25 +105,25 @@ def plan_bands(world: int, H: int, S: int, K: int = 8, h: int | None = None) -> 
             y1 = y0 + h + (h & 1)
             best = None
             while y1 <= H - rest * (h + (h & 1)):
-                if band_cost(y0, y1, H, S, K) <= T:
+                if band_cost(y0, y1, H, S, K, f32) <= T:
                     best = y1
                 y1 += 2
             if best is None:
                 return None
             cuts.append(best)
             y0 = best
-        if H - y0 < h or band_cost(y0, H, H, S, K) > T:
+        if H - y0 < h or band_cost(y0, H, H, S, K, f32) > T:
             return None
         return cuts + [H]
 
     def worst(cuts):
-        return max(band_cost(cuts[i], cuts[i + 1], H, S, K) for i in range(world))
+        return max(band_cost(cuts[i], cuts[i + 1], H, S, K, f32) for i in range(world))
 
     # band_cost is not monotone in y0 (the tile grid starts at y0 - 2), so greedy packing is not
     # optimal on its own: keep the best of the even split and the greedy plan.
     even = [2 * ((r * H) // (2 * world)) for r in range(world)] + [H]
     plans = [even] if min(even[i + 1] - even[i] for i in range(world)) >= h else []
-    lo_t, hi_t = 0.0, band_cost(0, H, H, S, K)          # feasibility of pack(T) is monotone in T
+    lo_t, hi_t = 0.0, band_cost(0, H, H, S, K, f32)          # feasibility of pack(T) is monotone in T
     best = pack(hi_t)
     for _ in range(40):
         mid = 0.5 * (lo_t + hi_t)
@@ -135,12 +139,12 @@ def plan_bands(world: int, H: int, S: int, K: int = 8, h: int | None = None) -> 
     return min(plans, key=worst)
 
 
-def band_of(rank: int, world: int, H: int, h: int, S: int | None = None, K: int = 8) -> Band:
+def band_of(rank: int, world: int, H: int, h: int, S: int | None = None, K: int = 8, f32: bool = False) -> Band:
     """Rank r's band: an even split of the rows, or (S given) the cost-balanced plan_bands split."""
     if world < 1 or not (0 <= rank < world):
         raise ValueError("bad rank/world")
     if S is not None and world > 1:
-        cuts = plan_bands(world, H, S, K, h)
+        cuts = plan_bands(world, H, S, K, h, f32)
         y0, y1 = cuts[rank], cuts[rank + 1]
     else:
         y0 = 2 * ((rank * H) // (2 * world))

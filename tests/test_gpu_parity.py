@@ -344,7 +344,7 @@ def test_f32_row_bands_equal_full_frame_config4(G):
         return fs, s.cpu().numpy().view(np.uint32)[y0 - b0:y1 - b0], cn.cpu().numpy()[y0 - b0:y1 - b0]
 
     full, fsum, fcnt = run(0, H, 0, H)
-    cuts = rowband.plan_bands(G, H, S, K)
+    cuts = rowband.plan_bands(G, H, S, K, f32=True)
     halo = rowband.halo_rows(S, K)
     for r in range(G):
         y0, y1 = cuts[r], cuts[r + 1]
@@ -846,10 +846,13 @@ def test_projection_only_mode(cfg):
                              fuse=qs.make_checks(), project=(pvs, pms, s, cn))
 
 
-@pytest.mark.parametrize("env,val,f32", [("QS_TMA", "1", True), ("QS_U8_BODY", "float", False)])
+@pytest.mark.parametrize("env,val,f32", [("QS_TMA", "1", True), ("QS_U8_BODY", "float", False),
+                                         ("QS_SPLIT", "0", True), ("QS_SPLIT", "2", True)])
 def test_staging_and_body_variants_bit_exact(env, val, f32, monkeypatch):
-    """The measured alternatives stay exact: TMA staging of the float window (QS_TMA=1) and the fp32
-    body for uint8 interior tiles (QS_U8_BODY=float) give the oracle's planes, interior and border."""
+    """The measured alternatives stay exact: TMA staging of the float window (QS_TMA=1), the fp32
+    body for uint8 interior tiles (QS_U8_BODY=float), and for float references me_box as one kernel
+    (QS_SPLIT=0) or as border / interior grids over the whole tile grid (QS_SPLIT=2) instead of the
+    default interior rectangle give the oracle's planes, interior and border."""
     monkeypatch.setenv(env, val)
     seq = synth.make_sequence(4 if f32 else 2, w=320, h=256)
     for t, d in ((5, 1), (6, 3)):

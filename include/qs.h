@@ -313,9 +313,12 @@ int qs_project(const qs_field *f, const uint8_t *past_val, const uint8_t *past_m
  * Launch timing (the profiling subsystem; SURVEY.md §5 "CUDA events per stage").
  * While enabled, every kernel launched by the entry points above is bracketed
  * by two CUDA events recorded on its own stream.  qs_profile_read synchronises
- * the recorded events and returns the summed device time and the launch count
- * of one kernel ("me_box", "epilogue", "finalize", "nnc", "revgrid", "rme_decide",
- * "project") or of all of them ("*").  qs_profile_reset drops the records.
+ * the recorded events and returns the summed device time and the number of
+ * bracketed launches of one kernel ("me_box", "epilogue", "finalize", "nnc",
+ * "revgrid", "rme_decide", "project", "certify") or of all of them ("*"); one
+ * bracket can hold several grids (certify: scan + fix; me_box on float
+ * references: the border grid and the interior grid).  qs_profile_reset drops
+ * the records.
  * Process-global; calls from several threads are serialised internally.
  * ------------------------------------------------------------------------- */
 int qs_profile_enable(int32_t on);

@@ -170,13 +170,23 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # QS_BENCH_BACKEND=gloo: a functional check of the N > 1 code path (row bands, halo exchange staged
+    # through host memory, max over ranks, the JSON line) when fewer GPUs than ranks exist -- ranks
+    # share GPUs round-robin, so its numbers are not a scaling measurement; the driver's runs use NCCL.
+    backend = os.environ.get("QS_BENCH_BACKEND", "nccl")
+    if backend not in ("nccl", "gloo"):
+        raise SystemExit(f"QS_BENCH_BACKEND={backend!r}: expected nccl or gloo")
+    gpu = local % torch.cuda.device_count() if backend == "gloo" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
         # NCCL's init lines (rank count, transports, NVLS) on stderr, so the rank count is checkable
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     cfg = synth.CONFIGS[args.config]
     W, H, K, S = cfg.w, cfg.h, cfg.K, cfg.S
     f32 = cfg.ref_f32
@@ -270,7 +280,7 @@ def run_ours(args):
     # in the refs and in_order modes (one stream) they time each kernel alone inside the timed region.
     qs.qs_profile_enable(True)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -302,7 +312,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         cms = c0.elapsed_time(c1)
         if world > 1:
-            tt = torch.tensor([cms], device=dev)
+            tt = torch.tensor([cms], device=dev if dist.get_backend() == "nccl" else "cpu")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             cms = float(tt.item())
         n_seq_c = world if args.sequences else 1
@@ -310,7 +320,7 @@ def run_ours(args):
                 "unit": "Mpixel/s", "ms_per_step": round(cms / args.steps, 4),
                 "how": "same steps, timed the same way, with the other pair schedule"}
     if world > 1:
-        tt = torch.tensor([ms], device=dev)
+        tt = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     n_seq = world if args.sequences else 1
@@ -376,6 +386,9 @@ def run_ours(args):
                           "mask": "dynamic" if cfg.dynamic else "fixed", "check": args.check,
                           "parallelism": (f"sequences{world}" if args.sequences else f"rowband{world}") if world > 1
                           else "single",
+                          **({"backend": f"gloo functional check: {world} ranks on "
+                                         f"{torch.cuda.device_count()} GPU(s), not a scaling number"}
+                             if backend != "nccl" and world > 1 else {}),
                           "pairs": {"refs": "one qs_me_search_refs call per step (ME, checks and PR of the "
                                             "three references: one me_box, one epilogue launch (+ certify for "
                                             "float references)); " + ("fields written" if args.fields else
@@ -503,7 +516,7 @@ def run_e2e(args, qs, torch, dist, world, band, frames, roi, prm, checks, dev, W
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     if world > 1:
-        tt = torch.tensor([ms], device=dev)
+        tt = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     n_seq = world if args.sequences else 1

@@ -169,15 +169,24 @@ def exchange_halo(plane: torch.Tensor, band: Band, group=None) -> None:
     own1 = band.y1 - band.b0          # buffer row one past the last owned row
     ops, landing = [], []
 
+    # gloo moves host memory only: device planes are staged through the host (the functional-check
+    # backend of bench.py and the CPU tests); NCCL sends device memory directly.
+    host = plane.is_cuda and dist.get_backend(group) == "gloo"
+
     def recv(rows):
         # pitched planes (row pitch > width) give non-contiguous row slices: receive into a
         # contiguous buffer and copy it in after the wait
-        dst = rows if rows.is_contiguous() else torch.empty(rows.shape, dtype=rows.dtype, device=rows.device)
+        if host:
+            dst = torch.empty(rows.shape, dtype=rows.dtype)
+        else:
+            dst = rows if rows.is_contiguous() else torch.empty(rows.shape, dtype=rows.dtype, device=rows.device)
         if dst is not rows:
             landing.append((rows, dst))
         return dst
 
     def send(rows):
+        if host:
+            return rows.cpu()
         return rows if rows.is_contiguous() else rows.contiguous()
 
     if r > 0:

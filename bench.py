@@ -368,6 +368,26 @@ def run_ours(args):
         roofline["int_alu"] = {"peak": ipk, "unit": "T int op/s", "frac": achieved / ipk,
                                "basis": "same 4 ops per (pixel, candidate) against the integer-ALU pipe peak "
                                         "(SURVEY.md 8(d.4) sanity ceiling; MEASURED_PEAKS_INT.json)"}
+    # Second kernel of the step (epilogue: finalize + NNC -> FRMC + PR): bound by shared-memory wavefronts
+    # (one per clock and SM); the wavefront count per launch is the committed ncu capture's
+    # (profiles/epilogue_pipes_c<cfg>.json; absent -> no entry), the launch time is measured live here.
+    ep_ms, ep_n = prof["epilogue"]
+    epath = os.path.join(ROOT, "profiles", f"epilogue_pipes_c{args.config}.json")
+    if ep_n and world == 1 and os.path.exists(epath):
+        try:
+            ep = json.load(open(epath))
+            wpk = SM_COUNT * SM_MAX_MHZ * 1e6 / 1e9
+            wav = ep["shared_wavefronts_per_launch"] / (ep_ms / ep_n / 1e3) / 1e9
+            use = (ep["shared_wavefronts_per_launch"] - ep["bank_conflict_wavefronts_per_launch"]) \
+                / (ep_ms / ep_n / 1e3) / 1e9
+            roofline["second"] = {"kernel": "epilogue", "bound": "shared", "achieved": wav, "peak": wpk,
+                                  "unit": "G wavefronts/s", "frac": wav / wpk,
+                                  "frac_without_bank_conflicts": use / wpk,
+                                  "avg_launch_ms": ep_ms / ep_n, "share_of_step": ep_ms / ms if ms else None,
+                                  "peak_basis": "148 SM x 1 shared-memory wavefront per clock x 1965 MHz",
+                                  "source": ep.get("source")}
+        except Exception:
+            pass
     kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
 
     e2e = None
